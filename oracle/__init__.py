@@ -1,0 +1,267 @@
+"""Parity oracle -- TEST INFRASTRUCTURE ONLY.
+
+Plain serial CPU implementation (``oracle/oracle.c``, plain C, integer only) of
+what the direction-optimized BFS hot path computes, plus thin numpy/ctypes
+wrappers.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import this package; the product
+package ``paper_1503_04359_b200`` never does, and shares no code with it.
+
+Citations: ``P:n`` = PAPER.md line n, ``S:n`` = SPEC.md line n.
+
+Functions and the passage each follows:
+
+* ``philox4x32_10``           -- counter-based RNG (R12)
+* ``kron_edges``              -- Graph500 Kronecker generator
+* ``build_csr``               -- CSR, each undirected edge as two arcs
+* ``degree_reindex`` / ``relabel_csr`` -- section 3.4 locality reindex
+* ``bfs``                     -- serial FIFO BFS, the plain definition
+* ``validate``                -- Graph500 validator V1-V6
+* ``do_emulate``              -- direction rule, counters, inspections
+* ``component_tuples``, ``compute_teps``, ``harmonic_mean`` -- TEPS
+* ``sample_roots``            -- seeded root list (R8)
+
+Parity status: every function above is pinned by ``tests/test_oracle_*.py``
+against values fixed independently of this code.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+KRON_ABC = (5700, 1900, 1900)  # Graph500 A, B, C per 10000
+ER_ABC = (2500, 2500, 2500)    # all quadrants equal: uniform random multigraph
+
+
+def build_library(force: bool = False) -> str:
+    """Compile oracle.c with gcc (plain -O2, no OpenMP, no vectorisation hints)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _L():
+    global _lib
+    with _lock:
+        if _lib is None:
+            lib = ctypes.CDLL(build_library())
+            i64, i32, u64, u32 = ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32
+            P = ctypes.c_void_p
+            lib.orc_philox4x32_10.argtypes = [P, P, P]
+            lib.orc_kron_scramble_keys.argtypes = [u64, P]
+            lib.orc_kron_scramble.argtypes = [i32, P, u32]
+            lib.orc_kron_scramble.restype = u32
+            lib.orc_kron_edges.argtypes = [i32, u64, u32, u32, u32, i64, i64, i32, P]
+            lib.orc_build_csr.argtypes = [i64, i64, P, i32, i32, i32, P, P, P]
+            lib.orc_build_csr.restype = i64
+            lib.orc_degree_reindex.argtypes = [i64, P, i64, P, P]
+            lib.orc_degree_reindex.restype = i32
+            lib.orc_relabel_csr.argtypes = [i64, P, P, P, P, P, P]
+            lib.orc_bfs.argtypes = [i64, P, P, i64, P, P]
+            lib.orc_bfs.restype = i64
+            lib.orc_validate.argtypes = [i64, P, P, i64, P, P, P, P, P]
+            lib.orc_validate.restype = i64
+            lib.orc_do_emulate.argtypes = [i64, P, P, P, i64, i64, i32, i64, i64, P, P, P, P, P, P, P]
+            lib.orc_do_emulate.restype = i64
+            lib.orc_component_tuples.argtypes = [i64, P, P]
+            lib.orc_component_tuples.restype = i64
+            lib.orc_sample_roots.argtypes = [i32, u64, i64, P, P, i64, i64, P]
+            lib.orc_sample_roots.restype = i64
+            _lib = lib
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _c(a, dtype):
+    return np.ascontiguousarray(a, dtype=dtype)
+
+
+# --------------------------------------------------------------------------- RNG / generator
+def philox4x32_10(ctr, key) -> np.ndarray:
+    """Philox4x32-10 of a 4-word counter under a 2-word key (Random123 definition)."""
+    c = _c(ctr, np.uint32)
+    k = _c(key, np.uint32)
+    out = np.zeros(4, np.uint32)
+    _L().orc_philox4x32_10(_p(c), _p(k), _p(out))
+    return out
+
+
+def scramble_keys(seed: int) -> np.ndarray:
+    out = np.zeros(4, np.uint32)
+    _L().orc_kron_scramble_keys(ctypes.c_uint64(seed), _p(out))
+    return out
+
+
+def scramble(scale: int, keys, v: int) -> int:
+    k = _c(keys, np.uint32)
+    return int(_L().orc_kron_scramble(scale, _p(k), v))
+
+
+def kron_edges(scale: int, edgefactor: int = 16, seed: int = 1, abc=KRON_ABC, first: int = 0,
+               count: int | None = None, scramble_labels: bool = True) -> np.ndarray:
+    """Edge tuples [first, first+count) of the Kronecker graph, int32 [count, 2]."""
+    m = edgefactor << scale
+    if count is None:
+        count = m - first
+    uv = np.zeros((count, 2), np.int32)
+    a, b, c = abc
+    _L().orc_kron_edges(scale, ctypes.c_uint64(seed), a, b, c, first, count, 1 if scramble_labels else 0, _p(uv))
+    return uv
+
+
+# --------------------------------------------------------------------------- CSR
+class CSR:
+    """offsets int64[n+1], adj int32[arcs]."""
+
+    def __init__(self, n: int, offsets: np.ndarray, adj: np.ndarray):
+        self.n = int(n)
+        self.offsets = offsets
+        self.adj = adj
+
+    @property
+    def arcs(self) -> int:
+        return int(self.offsets[-1])
+
+    def degree(self, v: int | None = None):
+        d = np.diff(self.offsets)
+        return d if v is None else int(d[v])
+
+    def row(self, v: int) -> np.ndarray:
+        return self.adj[self.offsets[v]:self.offsets[v + 1]]
+
+
+class MalformedInput(ValueError):
+    pass
+
+
+def build_csr(n: int, uv, dedup: bool = False, drop_self_loops: bool = False, sort_rows: bool = False) -> CSR:
+    """S:44-52 build_csr; raises MalformedInput naming the bad tuple."""
+    uv = _c(np.asarray(uv).reshape(-1, 2) if len(uv) else np.zeros((0, 2)), np.int32)
+    m = uv.shape[0]
+    offsets = np.zeros(n + 1, np.int64)
+    adj = np.zeros(max(2 * m, 1), np.int32)
+    arcs = np.zeros(1, np.int64)
+    rc = _L().orc_build_csr(n, m, _p(uv), int(dedup), int(drop_self_loops), int(sort_rows),
+                            _p(offsets), _p(adj), _p(arcs))
+    if rc < 0:
+        k = -rc - 1
+        raise MalformedInput(f"tuple {k} = ({uv[k, 0]}, {uv[k, 1]}) has an endpoint outside [0, {n})")
+    return CSR(n, offsets, adj[: int(arcs[0])].copy())
+
+
+def degree_reindex(g: CSR, p: int = 1):
+    """(new_label int64[n], position int64[n]) by (degree desc, ID asc), dealt round-robin to p parts."""
+    new_label = np.zeros(g.n, np.int64)
+    position = np.zeros(g.n, np.int64)
+    rc = _L().orc_degree_reindex(g.n, _p(g.offsets), p, _p(new_label), _p(position))
+    if rc != 0:
+        raise ValueError("p must divide n")
+    return new_label, position
+
+
+def relabel_csr(g: CSR, new_label: np.ndarray, position: np.ndarray) -> CSR:
+    offsets = np.zeros(g.n + 1, np.int64)
+    adj = np.zeros(max(g.arcs, 1), np.int32)
+    nl = _c(new_label, np.int64)
+    pos = _c(position, np.int64)
+    _L().orc_relabel_csr(g.n, _p(g.offsets), _p(g.adj), _p(nl), _p(pos), _p(offsets), _p(adj))
+    return CSR(g.n, offsets, adj[: g.arcs].copy())
+
+
+# --------------------------------------------------------------------------- BFS / validation
+def bfs(g: CSR, root: int):
+    """Serial FIFO BFS -> (depth int32[n], parent int32[n]); -1 = unreached."""
+    if not (0 <= root < g.n):
+        raise IndexError(f"root {root} outside [0, {g.n})")
+    depth = np.empty(g.n, np.int32)
+    parent = np.empty(g.n, np.int32)
+    _L().orc_bfs(g.n, _p(g.offsets), _p(g.adj if g.arcs else np.zeros(1, np.int32)), root, _p(depth), _p(parent))
+    return depth, parent
+
+
+RULES = ("V1_root", "V2_tree_edge", "V3_parent_depth", "V4_edge_span", "V5_unreached", "V6_exact_depth")
+
+
+def validate(g: CSR, root: int, depth, parent, ref_depth=None) -> dict:
+    """Graph500 validator; returns {rule: (fail_count, first_bad_vertex)} for failing rules only."""
+    d = _c(depth, np.int32)
+    p = _c(parent, np.int32)
+    r = _c(ref_depth, np.int32) if ref_depth is not None else None
+    fails = np.zeros(6, np.int64)
+    first = np.zeros(6, np.int64)
+    adj = g.adj if g.arcs else np.zeros(1, np.int32)
+    _L().orc_validate(g.n, _p(g.offsets), _p(adj), root, _p(d), _p(p), _p(r) if r is not None else None,
+                      _p(fails), _p(first))
+    return {RULES[i]: (int(fails[i]), int(first[i])) for i in range(6) if fails[i]}
+
+
+def do_emulate(g: CSR, depth, alpha: int = 15, beta: int = 18, policy: int = 0, bu_from: int = 0,
+               want_bu_parent: bool = False) -> dict:
+    """Per-step direction, n_f, m_f, m_u, discovered and inspections (see oracle.c)."""
+    d = _c(depth, np.int32)
+    S = int(d.max()) + 2 if d.size else 2
+    dirs = np.zeros(S, np.int32)
+    arrs = [np.zeros(S, np.int64) for _ in range(5)]
+    bp = np.zeros(g.n, np.int32) if want_bu_parent else None
+    adj = g.adj if g.arcs else np.zeros(1, np.int32)
+    steps = _L().orc_do_emulate(g.n, _p(g.offsets), _p(adj), _p(d), alpha, beta, policy, bu_from, S,
+                                _p(dirs), *[_p(a) for a in arrs], _p(bp) if bp is not None else None)
+    assert steps >= 0
+    out = {"dir": dirs[:steps], "n_f": arrs[0][:steps], "m_f": arrs[1][:steps], "m_u": arrs[2][:steps],
+           "discovered": arrs[3][:steps], "insp": arrs[4][:steps]}
+    if bp is not None:
+        out["bu_parent"] = bp
+    return out
+
+
+# --------------------------------------------------------------------------- TEPS
+def component_tuples(uv, depth) -> int:
+    uv = _c(np.asarray(uv).reshape(-1, 2), np.int32)
+    d = _c(depth, np.int32)
+    return int(_L().orc_component_tuples(uv.shape[0], _p(uv), _p(d)))
+
+
+def compute_teps(edges: int, seconds: float) -> float:
+    """edges / elapsed; elapsed must be > 0."""
+    if not seconds > 0:
+        raise ValueError("elapsed must be > 0")
+    return edges / seconds
+
+
+def harmonic_mean(rates) -> float:
+    """n / sum(1/rate); rates must be non-empty and positive."""
+    rates = list(rates)
+    if not rates or any(not r > 0 for r in rates):
+        raise ValueError("harmonic mean needs a non-empty list of positive rates")
+    return len(rates) / sum(1.0 / r for r in rates)
+
+
+def sample_roots(g: CSR, scale: int, seed: int, count: int = 64, max_candidates: int | None = None) -> np.ndarray:
+    if max_candidates is None:
+        max_candidates = max(64 * count, 4 * g.n)
+    roots = np.zeros(count, np.int64)
+    adj = g.adj if g.arcs else np.zeros(1, np.int32)
+    got = _L().orc_sample_roots(scale, ctypes.c_uint64(seed), g.n, _p(g.offsets), _p(adj), count,
+                                max_candidates, _p(roots))
+    return roots[:got]
+
+
+def kron_graph(scale: int, edgefactor: int = 16, seed: int = 1, abc=KRON_ABC, dedup: bool = True,
+               drop_self_loops: bool = True, sort_rows: bool = True):
+    """Convenience: (uv, CSR) of a generated graph, built entirely by the oracle."""
+    uv = kron_edges(scale, edgefactor, seed, abc)
+    return uv, build_csr(1 << scale, uv, dedup=dedup, drop_self_loops=drop_self_loops, sort_rows=sort_rows)
