@@ -1,0 +1,356 @@
+// The C ABI (include/bfs.h): argument checking, error model, handles.
+// Every entry point converts internal failures into bfs_status + a thread-local
+// message; nothing here computes on the host -- all work is in the kernels.
+#include <cstring>
+#include <exception>
+#include <new>
+#include <numeric>
+
+#include "internal.cuh"
+
+namespace bfsb {
+
+struct Failure {
+    bfs_status code;
+    std::string msg;
+};
+
+static thread_local std::string tl_error;
+
+void set_error(const std::string& msg) { tl_error = msg; }
+
+void fail(bfs_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+static void* (*g_alloc_fn)(size_t, void*, void*) = nullptr;
+static void (*g_free_fn)(void*, void*) = nullptr;
+static void* g_alloc_ctx = nullptr;
+
+void* dev_alloc(size_t bytes, cudaStream_t s) {
+    if (g_alloc_fn) {
+        void* p = g_alloc_fn(bytes, (void*)s, g_alloc_ctx);
+        if (!p) fail(BFS_ERR_OUT_OF_MEMORY, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
+        return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, s);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fail(e == cudaErrorMemoryAllocation ? BFS_ERR_OUT_OF_MEMORY : BFS_ERR_CUDA,
+             "device allocation of " + std::to_string(bytes) + " bytes failed (" + cudaGetErrorString(e) +
+                 "; free " + std::to_string(fr) + " of " + std::to_string(tot) + ")");
+    }
+    return p;
+}
+
+void dev_free(void* p, cudaStream_t s) {
+    if (!p) return;
+    if (g_free_fn) {
+        g_free_fn(p, g_alloc_ctx);
+        return;
+    }
+    cudaFreeAsync(p, s);  // errors here are not actionable (destructor path)
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a{};
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+int num_sms() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int v = 0;
+        BFS_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        cached[dev] = v > 0 ? v : 1;
+    }
+    return cached[dev];
+}
+
+static bfs_build_opts default_opts() { return bfs_build_opts{1, 1, 0, 1}; }
+
+}  // namespace bfsb
+
+using namespace bfsb;
+
+#define API_BEGIN try {
+#define API_END                                                   \
+    }                                                             \
+    catch (const Failure& f) {                                    \
+        set_error(f.msg);                                         \
+        return f.code;                                            \
+    }                                                             \
+    catch (const std::bad_alloc&) {                               \
+        set_error("host allocation failed");                      \
+        return BFS_ERR_OUT_OF_MEMORY;                             \
+    }                                                             \
+    catch (const std::exception& e) {                             \
+        set_error(std::string("internal error: ") + e.what());    \
+        return BFS_ERR_INTERNAL;                                  \
+    }                                                             \
+    catch (...) {                                                 \
+        set_error("internal error");                              \
+        return BFS_ERR_INTERNAL;                                  \
+    }                                                             \
+    return BFS_OK;
+
+extern "C" {
+
+int bfs_abi_version(void) { return BFS_ABI_VERSION; }
+
+const char* bfs_last_error(void) { return tl_error.c_str(); }
+
+bfs_status bfs_set_allocator(void* (*alloc_fn)(size_t, void*, void*), void (*free_fn)(void*, void*), void* ctx) {
+    API_BEGIN
+    if ((alloc_fn == nullptr) != (free_fn == nullptr)) fail(BFS_ERR_INVALID_ARG, "alloc_fn and free_fn must be both set or both NULL");
+    g_alloc_fn = alloc_fn;
+    g_free_fn = free_fn;
+    g_alloc_ctx = ctx;
+    API_END
+}
+
+bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* cuda_stream, bfs_graph_t* out) {
+    bfs_graph_s* g = nullptr;
+    API_BEGIN
+    if (!desc || !out) fail(BFS_ERR_INVALID_ARG, "desc and out must be non-NULL");
+    *out = nullptr;
+    if (comm) fail(BFS_ERR_INVALID_ARG, "multi-partition graphs are not available in this build");
+    bfs_graph_desc d = *desc;
+    int64_t n = d.n;
+    switch (d.kind) {
+        case BFS_SRC_KRONECKER:
+            validate_kron_spec(&d.kron);
+            n = (int64_t)1 << d.kron.scale;
+            break;
+        case BFS_SRC_EDGES:
+            if (d.m < 0) fail(BFS_ERR_INVALID_ARG, "m must be >= 0");
+            if (d.m > 0 && !d.uv) fail(BFS_ERR_INVALID_ARG, "uv is NULL");
+            break;
+        case BFS_SRC_CSR:
+            if (!d.offsets) fail(BFS_ERR_INVALID_ARG, "offsets is NULL");
+            break;
+        default:
+            fail(BFS_ERR_INVALID_ARG, "unknown source kind");
+    }
+    if (n < 1) fail(BFS_ERR_INVALID_ARG, "n must be >= 1");
+    if (n > 0x7fffffffLL) fail(BFS_ERR_CAPACITY, "n = " + std::to_string(n) + " exceeds int32 vertex IDs");
+    if (d.opts.reindex_by_degree) fail(BFS_ERR_INVALID_ARG, "reindex_by_degree is not available in this build");
+    g = new bfs_graph_s();
+    BFS_CUDA(cudaGetDevice(&g->device));
+    g->stream = (cudaStream_t)cuda_stream;
+    g->n = n;
+    g->lo = 0;
+    g->hi = n;
+    g->opts = d.opts;
+    cudaEvent_t e0, e1;
+    BFS_CUDA(cudaEventCreate(&e0));
+    BFS_CUDA(cudaEventCreate(&e1));
+    BFS_CUDA(cudaEventRecord(e0, g->stream));
+    build_graph(g, &d);
+    BFS_CUDA(cudaEventRecord(e1, g->stream));
+    BFS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BFS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    g->build_ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    bfs_alloc_state(g);
+    BFS_CUDA(cudaStreamSynchronize(g->stream));
+    *out = g;
+    g = nullptr;
+    }
+    catch (const Failure& f) {
+        delete g;
+        set_error(f.msg);
+        return f.code;
+    }
+    catch (...) {
+        delete g;
+        set_error("internal error during graph construction");
+        return BFS_ERR_INTERNAL;
+    }
+    return BFS_OK;
+}
+
+bfs_status bfs_graph_create_kronecker(const bfs_kron_spec* spec, const bfs_build_opts* opts, bfs_comm_t comm,
+                                      void* cuda_stream, bfs_graph_t* out) {
+    if (!spec) {
+        set_error("spec is NULL");
+        return BFS_ERR_INVALID_ARG;
+    }
+    bfs_graph_desc d{};
+    d.kind = BFS_SRC_KRONECKER;
+    d.kron = *spec;
+    d.opts = opts ? *opts : default_opts();
+    return bfs_graph_create(&d, comm, cuda_stream, out);
+}
+
+bfs_status bfs_graph_create_edges(const int32_t* uv, int64_t m, int64_t n, const bfs_build_opts* opts,
+                                  bfs_comm_t comm, void* cuda_stream, bfs_graph_t* out) {
+    bfs_graph_desc d{};
+    d.kind = BFS_SRC_EDGES;
+    d.uv = uv;
+    d.m = m;
+    d.n = n;
+    d.opts = opts ? *opts : default_opts();
+    return bfs_graph_create(&d, comm, cuda_stream, out);
+}
+
+bfs_status bfs_graph_create_csr(const int64_t* offsets, const int32_t* adj, int64_t n, const bfs_build_opts* opts,
+                                bfs_comm_t comm, void* cuda_stream, bfs_graph_t* out) {
+    bfs_graph_desc d{};
+    d.kind = BFS_SRC_CSR;
+    d.offsets = offsets;
+    d.adj = adj;
+    d.n = n;
+    d.opts = opts ? *opts : default_opts();
+    return bfs_graph_create(&d, comm, cuda_stream, out);
+}
+
+bfs_status bfs_graph_info(bfs_graph_t g, int64_t* n, int64_t* arcs, int64_t* local_begin, int64_t* local_end) {
+    API_BEGIN
+    if (!g) fail(BFS_ERR_INVALID_ARG, "graph is NULL");
+    if (n) *n = g->n;
+    if (arcs) *arcs = g->arcs_global;
+    if (local_begin) *local_begin = g->lo;
+    if (local_end) *local_end = g->hi;
+    API_END
+}
+
+bfs_status bfs_graph_build_ms(bfs_graph_t g, double* ms) {
+    API_BEGIN
+    if (!g || !ms) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    *ms = g->build_ms;
+    API_END
+}
+
+bfs_status bfs_set_policy(bfs_graph_t g, const bfs_policy* p) {
+    API_BEGIN
+    if (!g || !p) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    if (p->mode < 0 || p->mode > 2) fail(BFS_ERR_INVALID_ARG, "policy.mode must be 0, 1 or 2");
+    if (p->alpha < 1 || p->alpha > (1 << 24) || p->beta < 1 || p->beta > (1 << 24))
+        fail(BFS_ERR_INVALID_ARG, "alpha and beta must be in [1, 2^24]");
+    if (p->bu_from_level < 0) fail(BFS_ERR_INVALID_ARG, "bu_from_level must be >= 0");
+    g->policy = *p;
+    API_END
+}
+
+bfs_status bfs_run(bfs_graph_t g, int64_t root, int32_t* parent_out, int32_t* depth_out) {
+    API_BEGIN
+    if (!g) fail(BFS_ERR_INVALID_ARG, "graph is NULL");
+    BFS_CUDA(cudaSetDevice(g->device));
+    bfs_run_impl(g, root, parent_out, depth_out);
+    g->has_run = true;
+    API_END
+}
+
+bfs_status bfs_stats(bfs_graph_t g, bfs_run_stats* out, bfs_level_stats* levels, int max_levels) {
+    API_BEGIN
+    if (!g || !out) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    if (!g->has_run) fail(BFS_ERR_INVALID_ARG, "bfs_stats before any bfs_run");
+    BFS_CUDA(cudaSetDevice(g->device));
+    if (g->run.component_edge_tuples < 0) g->run.component_edge_tuples = component_tuples_impl(g);
+    *out = g->run;
+    if (levels)
+        for (int i = 0; i < max_levels && i < (int)g->levels.size(); ++i) levels[i] = g->levels[i];
+    API_END
+}
+
+bfs_status bfs_graph_destroy(bfs_graph_t g) {
+    API_BEGIN
+    if (!g) return BFS_OK;
+    cudaSetDevice(g->device);
+    cudaStreamSynchronize(g->stream);
+    for (auto& e : g->ev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : g->lev_ev) cudaEventDestroy(e);
+    if (g->h_cnt) cudaFreeHost(g->h_cnt);
+    delete g;
+    cudaDeviceSynchronize();
+    API_END
+}
+
+bfs_status bfs_comm_unique_id(uint8_t id[128]) {
+    (void)id;
+    set_error("multi-GPU communicator is not available in this build");
+    return BFS_ERR_NCCL;
+}
+
+bfs_status bfs_comm_create(int nranks, int rank, const uint8_t id[128], int device, bfs_comm_t* out) {
+    (void)nranks; (void)rank; (void)id; (void)device; (void)out;
+    set_error("multi-GPU communicator is not available in this build");
+    return BFS_ERR_NCCL;
+}
+
+bfs_status bfs_comm_create_local(int nparts, int device, bfs_comm_t* out) {
+    (void)nparts; (void)device; (void)out;
+    set_error("local multi-partition communicator is not available in this build");
+    return BFS_ERR_INVALID_ARG;
+}
+
+bfs_status bfs_comm_destroy(bfs_comm_t comm) {
+    (void)comm;
+    return BFS_OK;
+}
+
+bfs_status bfs_kronecker_edges(const bfs_kron_spec* spec, int64_t first, int64_t count, int32_t* uv_out,
+                               void* cuda_stream) {
+    API_BEGIN
+    if (!uv_out && count > 0) fail(BFS_ERR_INVALID_ARG, "uv_out is NULL");
+    if (count > 0 && !is_device_ptr(uv_out)) fail(BFS_ERR_INVALID_ARG, "uv_out must be device memory");
+    kron_edges_device(spec, first, count, uv_out, (cudaStream_t)cuda_stream);
+    BFS_CUDA(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+    API_END
+}
+
+bfs_status bfs_graph_export_csr(bfs_graph_t g, int64_t* offsets_out, int32_t* adj_out) {
+    API_BEGIN
+    if (!g) fail(BFS_ERR_INVALID_ARG, "graph is NULL");
+    BFS_CUDA(cudaSetDevice(g->device));
+    if (offsets_out)
+        BFS_CUDA(cudaMemcpyAsync(offsets_out, g->off.p, ((size_t)g->nl() + 1) * sizeof(int64_t), cudaMemcpyDefault,
+                                 g->stream));
+    if (adj_out && g->arcs_local)
+        BFS_CUDA(cudaMemcpyAsync(adj_out, g->adj.p, (size_t)g->arcs_local * sizeof(int32_t), cudaMemcpyDefault,
+                                 g->stream));
+    BFS_CUDA(cudaStreamSynchronize(g->stream));
+    API_END
+}
+
+bfs_status bfs_graph_export_labels(bfs_graph_t g, int32_t* new_label_out) {
+    API_BEGIN
+    if (!g || !new_label_out) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    BFS_CUDA(cudaSetDevice(g->device));
+    if (g->reindexed) {
+        BFS_CUDA(cudaMemcpyAsync(new_label_out, g->label.p, (size_t)g->n * 4, cudaMemcpyDefault, g->stream));
+    } else {
+        std::vector<int32_t> id((size_t)g->n);
+        std::iota(id.begin(), id.end(), 0);
+        BFS_CUDA(cudaMemcpyAsync(new_label_out, id.data(), (size_t)g->n * 4, cudaMemcpyDefault, g->stream));
+    }
+    BFS_CUDA(cudaStreamSynchronize(g->stream));
+    API_END
+}
+
+bfs_status bfs_sample_roots(bfs_graph_t g, uint32_t scale, uint64_t seed, int64_t count, int64_t* roots_out,
+                            int64_t* found) {
+    API_BEGIN
+    if (!g || !roots_out || !found) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    if (count < 0) fail(BFS_ERR_INVALID_ARG, "count must be >= 0");
+    if (scale > 31) fail(BFS_ERR_INVALID_ARG, "scale must be <= 31");
+    BFS_CUDA(cudaSetDevice(g->device));
+    sample_roots_impl(g, scale, seed, count, roots_out, found);
+    API_END
+}
+
+}  // extern "C"

@@ -1,0 +1,156 @@
+// Internal declarations shared by the library's translation units.
+// Product code only: nothing here is shared with oracle/ (DESIGN.md section 3).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/bfs.h"
+
+namespace bfsb {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+
+struct Error {
+    bfs_status code;
+    std::string msg;
+};
+
+// Throwing inside the library, converted to bfs_status at the C-ABI boundary.
+[[noreturn]] void fail(bfs_status code, const std::string& msg);
+
+#define BFS_CUDA(expr)                                                                          \
+    do {                                                                                        \
+        cudaError_t _e = (expr);                                                                \
+        if (_e != cudaSuccess)                                                                  \
+            ::bfsb::fail(_e == cudaErrorMemoryAllocation ? BFS_ERR_OUT_OF_MEMORY : BFS_ERR_CUDA, \
+                         std::string(#expr) + ": " + cudaGetErrorString(_e) + " (" __FILE__ ":" + \
+                             std::to_string(__LINE__) + ")");                                   \
+    } while (0)
+
+#define BFS_CHECK_LAUNCH() BFS_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------- memory
+void* dev_alloc(size_t bytes, cudaStream_t s);
+void dev_free(void* p, cudaStream_t s);
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t count = 0;
+    cudaStream_t s = nullptr;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept { *this = std::move(o); }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            p = o.p; count = o.count; s = o.s;
+            o.p = nullptr; o.count = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { reset(); }
+    void alloc(size_t n, cudaStream_t st) {
+        reset();
+        s = st;
+        count = n;
+        p = static_cast<T*>(dev_alloc((n ? n : 1) * sizeof(T), st));
+    }
+    void reset() {
+        if (p) dev_free(p, s);
+        p = nullptr;
+        count = 0;
+    }
+    size_t bytes() const { return count * sizeof(T); }
+};
+
+bool is_device_ptr(const void* p);
+
+// ---------------------------------------------------------------- geometry
+inline int64_t words_of(int64_t nbits) { return (nbits + 31) / 32; }
+// bitmap words padded to a multiple of 4 (16-byte vector access)
+inline int64_t padded_words(int64_t nbits) { return (words_of(nbits) + 3) / 4 * 4; }
+
+int num_sms();
+
+// ---------------------------------------------------------------- scan (scan.cu)
+// out[i] = sum_{k<i} f(k) for i in [0, n], i.e. n+1 outputs (out[n] = total).
+// Input is int32 or int64 array; out may alias in only when both are int64.
+int scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
+int scan_exclusive_i32(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);
+// out[i] for i in [0, F]: prefix of row lengths of queue entries q[i] (degree of q[i]),
+// len(q[i]) = off[q[i]-lo+1] - off[q[i]-lo]
+int scan_queue_degrees(const int32_t* q, int64_t F, const int64_t* off, int64_t lo, int64_t* out,
+                        cudaStream_t s);
+
+// ---------------------------------------------------------------- communication (comm.cu)
+struct Comm;  // NCCL-backed or local-simulated; defined in comm.cu
+
+}  // namespace bfsb
+
+// ---------------------------------------------------------------- the handle
+struct bfs_graph_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int64_t n = 0;          // global vertices
+    int64_t lo = 0, hi = 0; // owned internal-label range (whole graph on one GPU)
+    int64_t arcs_local = 0; // arcs stored on this rank
+    int64_t arcs_global = 0;
+    int64_t tuples = 0;     // raw input tuples
+    double build_ms = 0;
+    bfs_build_opts opts{};
+    bfs_comm_t comm = nullptr;
+    int nparts = 1;         // partitions held by this process (>1 only for a local comm)
+    int part0 = 0;          // first partition index held here
+
+    // CSR of owned rows (internal labels); adjacency holds global internal IDs
+    bfsb::DevBuf<int64_t> off;      // [nl + 1]
+    bfsb::DevBuf<int32_t> adj;      // [arcs_local]
+    bfsb::DevBuf<int32_t> deg_raw;  // [nl] raw arcs per vertex (TEPS numerator)
+    bfsb::DevBuf<uint32_t> skip;    // [padded words of nl] bit set = CSR degree 0
+    // reindex (identity when absent)
+    bool reindexed = false;
+    bfsb::DevBuf<int32_t> label;    // [n] original -> internal
+    bfsb::DevBuf<int32_t> ilabel;   // [n] internal -> original
+
+    // BFS state
+    bfsb::DevBuf<uint32_t> visited;  // [padded words of nl]
+    bfsb::DevBuf<uint32_t> front;    // [padded words of n] global frontier bitmap
+    bfsb::DevBuf<uint32_t> next;     // [padded words of n] global next bitmap
+    bfsb::DevBuf<int32_t> q0, q1;    // [nl] frontier queues (global internal IDs)
+    bfsb::DevBuf<int64_t> prefix;    // [nl + 1] TD degree prefix
+    bfsb::DevBuf<int64_t> cnt;       // [8] device counters
+    int64_t* h_cnt = nullptr;        // pinned mirror
+    bfsb::DevBuf<int32_t> tmp_depth, tmp_parent;  // internal-label outputs / host staging
+    bfsb::DevBuf<int64_t> scratch64; // small reductions
+
+    bfs_policy policy{0, 15, 18, 0, 0};
+    std::vector<bfs_level_stats> levels;
+    bfs_run_stats run{};
+    int64_t last_root_l = 0;
+    bool has_run = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    std::vector<cudaEvent_t> lev_ev;
+
+    int64_t nl() const { return hi - lo; }
+};
+
+namespace bfsb {
+// build.cu
+void build_graph(bfs_graph_s* g, const bfs_graph_desc* d);
+void kron_edges_device(const bfs_kron_spec* spec, int64_t first, int64_t count, int32_t* uv, cudaStream_t s);
+void validate_kron_spec(const bfs_kron_spec* spec);
+// bfs.cu
+void bfs_alloc_state(bfs_graph_s* g);
+void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out);
+int64_t component_tuples_impl(bfs_graph_s* g);
+void sample_roots_impl(bfs_graph_s* g, uint32_t scale, uint64_t seed, int64_t count, int64_t* roots, int64_t* found);
+// host-side Philox (product's own; used for root candidates)
+void philox4x32_10_host(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+}  // namespace bfsb

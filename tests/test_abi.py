@@ -1,0 +1,67 @@
+"""CPU-side checks of the C ABI: the library builds, loads, exports every symbol
+include/bfs.h declares, and fails loudly (not silently) without a GPU."""
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_1503_04359_b200 as pkg
+from paper_1503_04359_b200 import build as b
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def so():
+    return b.build()
+
+
+def _header_functions():
+    txt = open(os.path.join(ROOT, "include", "bfs.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return set(re.findall(r"\b(bfs_[a-z_0-9]+)\s*\(", txt))
+
+
+def test_header_declares_what_binding_exports():
+    assert _header_functions() == set(pkg.EXPORTS)
+
+
+def test_library_exports_every_symbol(so):
+    out = subprocess.run(["nm", "-D", "--defined-only", so], capture_output=True, text=True, check=True).stdout
+    syms = {line.split()[-1] for line in out.splitlines() if line.strip()}
+    missing = _header_functions() - syms
+    assert not missing, missing
+
+
+def test_library_loads_and_reports_version(so):
+    L = pkg.lib()
+    assert L.bfs_abi_version() == 1
+    for name in pkg.EXPORTS:
+        assert hasattr(L, name)
+
+
+def test_no_oracle_in_product_sources():
+    """The product package never imports or links the oracle."""
+    pkg_dir = os.path.join(ROOT, "paper_1503_04359_b200")
+    for dirpath, _, files in os.walk(pkg_dir):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt, f
+                assert "oracle.c" not in txt and "liboracle" not in txt, f
+
+
+def test_errors_are_reported_not_swallowed(so):
+    import ctypes
+    try:
+        import torch
+        if torch.cuda.is_available():
+            pytest.skip("CPU-only check")
+    except Exception:
+        pass
+    h = ctypes.c_void_p()
+    st = pkg.lib().bfs_graph_create_kronecker(None, None, None, None, ctypes.byref(h))
+    assert st == 1 and b"NULL" in pkg.lib().bfs_last_error()
+    with pytest.raises(pkg.BfsError):
+        pkg.bfs_graph_create_kronecker(8)   # no device here -> BFS_ERR_CUDA, never a CPU fallback

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by
+element, on the same seeded inputs.
+
+Bars: generator tuples, CSR offsets/adjacency, depth,
+roots, counters and inspection counts are bit-exact; parents may differ from
+the oracle's FIFO tree and must pass the Graph500 validator, except for
+vertices discovered by bottom-up steps, whose parent is unique (first frontier
+neighbour in row order) and must equal the emulator's.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from tests import graphs
+
+torch = pytest.importorskip("torch")
+pkg = pytest.importorskip("paper_1503_04359_b200")
+from paper_1503_04359_b200 import build as pkg_build  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+POLICIES = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=2, bu_from_level=0),
+            dict(mode=0, alpha=2, beta=4), dict(mode=0, alpha=100, beta=2)]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    pkg_build.build()
+    torch.cuda.set_device(0)
+
+
+def _gpu_csr(g):
+    off, adj = g.export_csr()
+    return off.cpu().numpy(), adj.cpu().numpy()
+
+
+def _check_run(g, ref, root, policy, uv=None):
+    g.set_policy(**policy)
+    parent, depth = g.run(int(root))
+    d = depth.cpu().numpy()
+    p = parent.cpu().numpy()
+    want, _ = oracle.bfs(ref, int(root))
+    assert np.array_equal(d, want), f"depth mismatch root={root} policy={policy}: " \
+                                    f"{np.nonzero(d != want)[0][:10]}"
+    bad = oracle.validate(ref, int(root), d, p, ref_depth=want)
+    assert not bad, bad
+    emu = oracle.do_emulate(ref, want, alpha=policy.get("alpha", 15), beta=policy.get("beta", 18),
+                            policy=policy.get("mode", 0), bu_from=policy.get("bu_from_level", 0),
+                            want_bu_parent=True)
+    run, levels = g.stats()
+    assert run["levels"] == len(emu["insp"])
+    for key, lk in (("dir", "direction"), ("n_f", "frontier"), ("discovered", "discovered"), ("m_f", "m_f"),
+                    ("m_u", "m_u"), ("insp", "inspections")):
+        assert [lv[lk] for lv in levels] == emu[key].tolist(), (key, root, policy)
+    bu = emu["bu_parent"] >= 0
+    assert np.array_equal(p[bu], emu["bu_parent"][bu]), "bottom-up parent is not the first frontier neighbour"
+    assert run["reached"] == int((want >= 0).sum())
+    if uv is not None:
+        assert run["component_edge_tuples"] == oracle.component_tuples(uv, want)
+    return run, levels
+
+
+# ------------------------------------------------------------------ generator
+@pytest.mark.parametrize("scale,ef,seed,abc", [(1, 1, 42, oracle.KRON_ABC), (10, 16, 7, oracle.KRON_ABC),
+                                               (16, 16, 1, oracle.KRON_ABC), (13, 8, 3, oracle.ER_ABC),
+                                               (20, 1, 5, oracle.KRON_ABC)])
+def test_generator_bit_exact(scale, ef, seed, abc):
+    m = ef << scale
+    uv = torch.empty((m, 2), dtype=torch.int32, device="cuda")
+    pkg.bfs_kronecker_edges(scale, ef, seed, abc, 0, m, uv)
+    want = oracle.kron_edges(scale, ef, seed, abc)
+    assert np.array_equal(uv.cpu().numpy(), want)
+
+
+def test_generator_range_offsets():
+    scale, ef, seed = 12, 16, 9
+    uv = torch.empty((777, 2), dtype=torch.int32, device="cuda")
+    pkg.bfs_kronecker_edges(scale, ef, seed, oracle.KRON_ABC, 5000, 777, uv)
+    assert np.array_equal(uv.cpu().numpy(), oracle.kron_edges(scale, ef, seed, first=5000, count=777))
+
+
+# ------------------------------------------------------------------ CSR
+@pytest.mark.parametrize("dedup,loops,sort", [(1, 1, 1), (0, 0, 1), (1, 0, 1), (0, 1, 1)])
+def test_csr_kronecker_bit_exact(dedup, loops, sort):
+    scale = 14
+    opts = pkg.default_opts(dedup, loops, False, sort)
+    g = pkg.Graph.kronecker(scale, 16, 3, opts=opts)
+    off, adj = _gpu_csr(g)
+    uv = oracle.kron_edges(scale, 16, 3)
+    ref = oracle.build_csr(1 << scale, uv, dedup=bool(dedup), drop_self_loops=bool(loops), sort_rows=True)
+    assert np.array_equal(off, ref.offsets)
+    assert np.array_equal(adj, ref.adj)
+    g.close()
+
+
+def test_csr_unsorted_row_multisets():
+    n, uv = graphs.skewed_edges(5000, 60000, 2)
+    g = pkg.Graph.from_edges(torch.from_numpy(uv), n, opts=pkg.default_opts(False, False, False, False))
+    off, adj = _gpu_csr(g)
+    ref = oracle.build_csr(n, uv, sort_rows=True)
+    assert np.array_equal(off, ref.offsets)
+    for v in range(0, n, 7):
+        assert sorted(adj[off[v]:off[v + 1]].tolist()) == ref.row(v).tolist()
+    g.close()
+
+
+def test_csr_big_rows_merge_path():
+    """rows longer than the 32768-element shared-memory sort go through the merge passes"""
+    rng = np.random.default_rng(11)
+    n = 1 << 20
+    hub_edges = np.stack([np.zeros(200000, np.int64), rng.integers(0, n, 200000)], 1)
+    hub2 = np.stack([np.full(70000, 5), rng.integers(0, n, 70000)], 1)
+    rest = rng.integers(0, n, size=(300000, 2))
+    uv = np.concatenate([hub_edges, hub2, rest]).astype(np.int32)
+    for opts in ((1, 1, 0, 1), (0, 0, 0, 1)):
+        g = pkg.Graph.from_edges(torch.from_numpy(uv).cuda(), n, opts=pkg.default_opts(*opts))
+        off, adj = _gpu_csr(g)
+        ref = oracle.build_csr(n, uv, dedup=bool(opts[0]), drop_self_loops=bool(opts[1]), sort_rows=True)
+        assert np.array_equal(off, ref.offsets) and np.array_equal(adj, ref.adj)
+        g.close()
+
+
+def test_csr_input_path():
+    n, uv = graphs.skewed_edges(3000, 20000, 4)
+    ref = oracle.build_csr(n, uv)
+    g = pkg.Graph.from_csr(ref.offsets, ref.adj, n)
+    off, adj = _gpu_csr(g)
+    want = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    assert np.array_equal(off, want.offsets) and np.array_equal(adj, want.adj)
+    g.close()
+
+
+def test_malformed_inputs():
+    with pytest.raises(pkg.BfsError, match="MALFORMED.*tuple 1 = \\(2, 5\\)"):
+        pkg.Graph.from_edges(np.array([[0, 1], [2, 5]], np.int32), 5)
+    with pytest.raises(pkg.BfsError, match="CAPACITY"):
+        pkg.Graph.kronecker(31)
+
+
+# ------------------------------------------------------------------ BFS
+FIXTURES = {
+    "g1": graphs.g1(), "path": graphs.path(40), "cycle": graphs.cycle(33), "star": graphs.star(70),
+    "clique": graphs.clique(20), "bip": graphs.complete_bipartite(5, 9), "cube": graphs.hypercube(7),
+    "grid": graphs.grid(13, 17), "heap": graphs.heap_tree(300),
+    "union": graphs.disjoint_union(graphs.path(6), graphs.cycle(5), graphs.star(40), graphs.clique(7)),
+    "skewed": graphs.skewed_edges(3000, 20000, 1), "random": graphs.random_edges(2000, 9000, 3),
+}
+
+
+@pytest.mark.parametrize("name", sorted(FIXTURES))
+@pytest.mark.parametrize("pi", range(len(POLICIES)))
+def test_fixtures_all_policies(name, pi):
+    n, uv = FIXTURES[name]
+    g = pkg.Graph.from_edges(uv, n)
+    ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    for root in sorted({0, n // 2, n - 1, int(np.argmax(ref.degree()))}):
+        _check_run(g, ref, root, POLICIES[pi], uv)
+    g.close()
+
+
+def test_g1_golden_trace():
+    want = graphs.load_golden_table("g1_do_trace.txt")
+    n, uv = graphs.g1()
+    g = pkg.Graph.from_edges(uv, n)
+    g.set_policy(mode=0)
+    parent, depth = g.run(0)
+    assert depth.cpu().tolist() == [0, 1, 1, 1, 2, 3]
+    assert parent.cpu().tolist() == want["auto_parent"]
+    _, levels = g.stats()
+    assert [lv["inspections"] for lv in levels] == want["auto_insp"]
+    g.set_policy(mode=1)
+    g.run(0)
+    _, levels = g.stats()
+    assert [lv["inspections"] for lv in levels] == want["td_insp"]
+    g.close()
+
+
+def test_isolated_root_and_out_of_range():
+    g = pkg.Graph.from_edges(np.array([[0, 1], [1, 2]], np.int32), 6)
+    parent, depth = g.run(4)
+    assert depth.cpu().tolist() == [-1, -1, -1, -1, 0, -1]
+    assert parent.cpu().tolist() == [-1, -1, -1, -1, 4, -1]
+    run, levels = g.stats()
+    assert run["levels"] == 1 and run["reached"] == 1 and run["component_edge_tuples"] == 0
+    with pytest.raises(pkg.BfsError, match="OUT_OF_RANGE"):
+        g.run(6)
+    g.close()
+
+
+def test_self_loops_and_multi_edges_kept():
+    n, uv = graphs.grid(9, 9)
+    uv2 = np.concatenate([uv, uv[::2], np.array([[v, v] for v in range(0, n, 3)], np.int32)])
+    g = pkg.Graph.from_edges(uv2, n, opts=pkg.default_opts(False, False, False, True))
+    ref = oracle.build_csr(n, uv2, sort_rows=True)
+    for pol in POLICIES:
+        _check_run(g, ref, 40, pol, uv2)
+    g.close()
+
+
+@pytest.mark.parametrize("abc,seed", [(oracle.KRON_ABC, 1), (oracle.ER_ABC, 2)])
+def test_s16_64_roots(abc, seed):
+    scale = 16
+    g = pkg.Graph.kronecker(scale, 16, seed, abc)
+    uv, ref = oracle.kron_graph(scale, 16, seed, abc)
+    off, adj = _gpu_csr(g)
+    assert np.array_equal(off, ref.offsets) and np.array_equal(adj, ref.adj)
+    roots = g.sample_roots(scale, seed, 64)
+    assert np.array_equal(roots, oracle.sample_roots(ref, scale, seed, 64))
+    for i, r in enumerate(roots):
+        _check_run(g, ref, r, POLICIES[i % 3] if i < 12 else POLICIES[0], uv)
+    g.close()
+
+
+def test_host_output_buffers():
+    """the end-to-end path: outputs in (pinned or pageable) host memory"""
+    scale = 13
+    g = pkg.Graph.kronecker(scale, 16, 4)
+    uv, ref = oracle.kron_graph(scale, 16, 4)
+    r = int(g.sample_roots(scale, 4, 1)[0])
+    d = np.empty(1 << scale, np.int32)
+    p = torch.empty(1 << scale, dtype=torch.int32).pin_memory()
+    pkg.bfs_run(g.h, r, p, d)
+    want, _ = oracle.bfs(ref, r)
+    assert np.array_equal(d, want)
+    assert not oracle.validate(ref, r, d, p.numpy(), ref_depth=want)
+    g.close()
+
+
+def test_repeated_runs_and_stream():
+    s = torch.cuda.Stream()
+    scale = 14
+    g = pkg.Graph.kronecker(scale, 16, 6, stream=s)
+    uv, ref = oracle.kron_graph(scale, 16, 6)
+    roots = g.sample_roots(scale, 6, 5)
+    for _ in range(2):
+        for r in roots:
+            with torch.cuda.stream(s):
+                parent, depth = g.run(int(r))
+            s.synchronize()
+            want, _ = oracle.bfs(ref, int(r))
+            assert np.array_equal(depth.cpu().numpy(), want)
+    g.close()
