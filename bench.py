@@ -223,16 +223,30 @@ def main():
     from paper_1503_04359_b200 import build as pkg_build
 
     ws, rank, local = dist_env()
-    pkg_build.build()
+    if rank == 0:
+        pkg_build.build()
     torch.cuda.set_device(local)
+    comm = None
+    dist = None
     if ws > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        raise SystemExit("multi-GPU bench path lands with the partitioned engine (DESIGN.md section 7)")
+        dist.barrier()
+        pkg_build.build()   # no-op when rank 0 already built it
+        uid = pkg.bfs_comm_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device="cuda")
+        dist.broadcast(t, 0)
+        comm = pkg.bfs_comm_create(ws, rank, bytes(t.cpu().tolist()), local)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
 
     cfg = CONFIGS[args.config]
     stream = torch.cuda.Stream()
-    g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], stream=stream)
+    g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], comm=comm, stream=stream)
     build_ms = g.build_ms
     roots = g.sample_roots(cfg["scale"], cfg["seed"], args.roots)
     n = g.n
@@ -258,20 +272,19 @@ def main():
             if int(r) not in edges:
                 edges[int(r)] = g.stats()[0]["component_edge_tuples"]
 
-    times, rates, launches, step_ms = [], [], 0, []
+    times, launches = [], 0
     kern = {"bu": [0.0, 0, 0], "td": [0.0, 0, 0]}   # ms, bytes, launches
     levels_dump = []
-    torch.cuda.synchronize()
+    nvl_level_bytes = []
+    barrier()
     with ClockSampler(local) as clk:
         for step in range(args.steps):
-            s_ms = 0.0
             for r in roots:
                 ms = one(r)
                 run, levels = g.stats()
-                s_ms += ms
                 times.append(ms)
-                rates.append(edges[int(r)] / (ms * 1e-3) / 1e9)
                 launches += run["kernel_launches"]
+                nvl_level_bytes += [lv["nvlink_bytes"] for lv in levels]
                 for lv in levels:
                     key = "bu" if lv["direction"] == 1 else "td"
                     if key == "td" and lv["m_f"] == 0:
@@ -281,8 +294,13 @@ def main():
                     kern[key][2] += 1
                 if step == 0:
                     levels_dump.append({"root": int(r), "ms": ms, "levels": levels})
-            step_ms.append(s_ms)
-        torch.cuda.synchronize()
+        barrier()
+    if dist is not None:   # per-BFS time = max over ranks
+        tt = torch.tensor(times, dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        times = tt.cpu().tolist()
+    rates = [edges[int(roots[i % len(roots)])] / (ms * 1e-3) / 1e9 for i, ms in enumerate(times)]
+    step_ms = [sum(times[k * len(roots):(k + 1) * len(roots)]) for k in range(args.steps)]
     value = hmean(rates)
     clocks = clk.summary()
 
@@ -295,7 +313,7 @@ def main():
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("k_bu_step" if dom == "bu" else "k_td_expand")
+            traffic = json.load(f).get("k_bu_batch" if dom == "bu" else "k_td_expand")
     total_ms = sum(times)
     share = kms / total_ms if total_ms else 0.0
 
@@ -314,15 +332,19 @@ def main():
             ev1.record(stream)
             ev1.synchronize()
             e_rates.append(edges[int(r)] / (ev0.elapsed_time(ev1) * 1e-3) / 1e9)
+        if dist is not None:
+            et = torch.tensor([edges[int(r)] / x for r, x in zip(roots, e_rates)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(et, op=dist.ReduceOp.MAX)      # seconds*1e9 per BFS, max over ranks
+            e_rates = [edges[int(r)] / x for r, x in zip(roots, et.cpu().tolist())]
         e2e = {"value": round(hmean(e_rates), 4), "unit": "GTEPS", "h2d_bytes_per_step": 8 * len(roots),
-               "d2h_bytes_per_step": 8 * nl * len(roots),
+               "d2h_bytes_per_step": 8 * nl * len(roots) * ws,
                "note": "bfs_run with pinned host parent/depth buffers; root passed by value"}
 
     if args.levels_out:
         with open(args.levels_out, "w") as f:
             json.dump(levels_dump, f)
 
-    cpu = None if args.no_cpu_baseline else cpu_baseline_record()
+    cpu = None if (args.no_cpu_baseline or ws > 1) else cpu_baseline_record()
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 4), "higher_is_better": True,
@@ -334,12 +356,16 @@ def main():
         "per_root_ms": {"min": round(min(times), 4), "median": round(statistics.median(times), 4),
                         "max": round(max(times), 4)},
         "gteps_min_median_max": [round(min(rates), 3), round(statistics.median(rates), 3), round(max(rates), 3)],
-        "roofline": {"bound": "hbm", "kernel": "k_bu_step" if dom == "bu" else "k_td_expand",
+        "roofline": {"bound": "hbm", "kernel": "k_bu_batch" if dom == "bu" else "k_td_expand",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "share_of_step": round(share, 4), "launches": klaunch,
                      "bytes_per_launch": int(kbytes / klaunch) if klaunch else 0},
         "gpu_launches": launches,
+        "nvlink": None if ws == 1 else {
+            "bytes_per_level_max": max(nvl_level_bytes) if nvl_level_bytes else 0,
+            "bytes_per_bfs_mean": sum(nvl_level_bytes) / max(1, len(times)),
+            "link_gbs_ref": 900.0, "note": "bytes this rank sent to peers (rank 0)"},
         "clocks": clocks,
         "e2e": e2e,
         "cpu_baseline": cpu,
@@ -347,6 +373,9 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     g.close()
+    if comm is not None:
+        pkg.bfs_comm_destroy(comm)
+        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

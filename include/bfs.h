@@ -184,17 +184,30 @@ bfs_status bfs_stats(bfs_graph_t g, bfs_run_stats* out, bfs_level_stats* levels,
 bfs_status bfs_graph_destroy(bfs_graph_t g);
 
 /* ---- multi-GPU (SURVEY e; Alg. 2/3) ----
- * One process per GPU.  Rank 0 calls bfs_comm_unique_id and ships the 128 bytes
- * to the other ranks (e.g. torch.distributed broadcast); every rank then calls
+ * 1D vertex partition: rank r owns [r*nb, min(n, (r+1)*nb)) with
+ * nb = ceil(ceil(n/p)/32)*32 (bfs_partition_range).  Per level, bottom-up steps
+ * allgather the next-frontier bitmap slices (Alg. 3 PullFrontiers); top-down steps
+ * send (vertex, parent) claims for remote vertices to their owners with grouped
+ * send/recv after an allgather of the p x p claim counts (Alg. 2 PushFrontiers);
+ * the four switch counters are allreduced, so every rank takes the same direction.
+ * Parents travel with the top-down claims, so no separate aggregation step is
+ * needed (contrast P:79).
+ * One process per GPU: rank 0 calls bfs_comm_unique_id and ships the 128 bytes to
+ * the other ranks (e.g. torch.distributed broadcast); every rank then calls
  * bfs_comm_create with its rank and CUDA device.  NCCL is loaded at run time
- * (dlopen "libnccl.so.2"); BFS_ERR_NCCL if it is unavailable. */
+ * (dlopen "libnccl.so.2"); BFS_ERR_NCCL if it is unavailable.  Every rank must
+ * issue the same sequence of graph / run / stats calls (collective semantics). */
 bfs_status bfs_comm_unique_id(uint8_t id[128]);
 bfs_status bfs_comm_create(int nranks, int rank, const uint8_t id[128], int device, bfs_comm_t* out);
-/* Testing aid: p partitions simulated inside ONE process on ONE device; the
- * per-level exchange is done with device copies instead of NCCL.  A graph built
- * with such a comm holds all p partitions and bfs_run returns all n outputs. */
+/* Testing aid: out[0..nparts) receives nparts rank endpoints that live in ONE
+ * process on ONE device and exchange through device copies instead of NCCL.  Each
+ * endpoint is driven from its own host thread exactly like a separate process
+ * (same calls, same kernels, same host logic); only the transport differs. */
 bfs_status bfs_comm_create_local(int nparts, int device, bfs_comm_t* out);
 bfs_status bfs_comm_destroy(bfs_comm_t comm);
+/* Host arithmetic only (no device needed): the vertex range rank `rank` of
+ * `nranks` owns for an n-vertex graph. */
+bfs_status bfs_partition_range(int64_t n, int nranks, int rank, int64_t* local_begin, int64_t* local_end);
 
 const char* bfs_last_error(void);
 

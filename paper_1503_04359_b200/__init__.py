@@ -32,7 +32,7 @@ EXPORTS = ("bfs_graph_create", "bfs_graph_create_kronecker", "bfs_graph_create_e
            "bfs_graph_info", "bfs_graph_build_ms", "bfs_set_policy", "bfs_run", "bfs_stats", "bfs_graph_destroy",
            "bfs_comm_unique_id", "bfs_comm_create", "bfs_comm_create_local", "bfs_comm_destroy", "bfs_last_error",
            "bfs_kronecker_edges", "bfs_graph_export_csr", "bfs_graph_export_labels", "bfs_sample_roots",
-           "bfs_set_allocator", "bfs_abi_version")
+           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range")
 
 
 class BfsError(RuntimeError):
@@ -109,6 +109,7 @@ def lib() -> ctypes.CDLL:
             "bfs_graph_export_labels": [P, P],
             "bfs_sample_roots": [P, ctypes.c_uint32, ctypes.c_uint64, i64, P, P],
             "bfs_set_allocator": [P, P, P],
+            "bfs_partition_range": [i64, i32, i32, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -245,10 +246,41 @@ def bfs_comm_create(nranks: int, rank: int, uid: bytes, device: int) -> ctypes.c
     return h
 
 
-def bfs_comm_create_local(nparts: int, device: int = 0) -> ctypes.c_void_p:
-    h = ctypes.c_void_p()
-    _check(lib().bfs_comm_create_local(nparts, device, ctypes.byref(h)))
-    return h
+def bfs_comm_create_local(nparts: int, device: int = 0) -> list:
+    """nparts rank endpoints in this process (one device); drive each from its own thread."""
+    arr = (ctypes.c_void_p * nparts)()
+    _check(lib().bfs_comm_create_local(nparts, device, arr))
+    return [ctypes.c_void_p(arr[i]) for i in range(nparts)]
+
+
+def bfs_partition_range(n: int, nranks: int, rank: int):
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().bfs_partition_range(n, nranks, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def run_ranks(fn, nranks: int):
+    """Call fn(rank) on nranks host threads (for local-comm partitions); re-raise the
+    first failure.  ctypes releases the GIL inside library calls, so the ranks
+    progress concurrently through their collectives."""
+    import threading
+    out = [None] * nranks
+    err = []
+
+    def body(r):
+        try:
+            out[r] = fn(r)
+        except BaseException as e:  # noqa: BLE001
+            err.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(nranks)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if err:
+        raise err[0]
+    return out
 
 
 def bfs_comm_destroy(h):

@@ -21,8 +21,24 @@ LIB = os.path.join(HERE, "libbfsb200.so")
 OBJDIR = os.path.join(HERE, "build_obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+
+
+def _nccl_include() -> str:
+    """nccl.h for types only (the library dlopens libnccl.so.2 at run time)."""
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    if os.path.exists("/usr/include/nccl.h"):
+        return "/usr/include"
+    raise RuntimeError("nccl.h not found")
+
 NVCC_FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",
-              "-Xptxas", "-v", "-I", INCLUDE] + ARCH
+              "-Xptxas", "-v", "-I", INCLUDE, "-I", _nccl_include()] + ARCH
 
 
 def _nvcc() -> str:

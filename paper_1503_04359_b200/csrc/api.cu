@@ -124,7 +124,6 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
     API_BEGIN
     if (!desc || !out) fail(BFS_ERR_INVALID_ARG, "desc and out must be non-NULL");
     *out = nullptr;
-    if (comm) fail(BFS_ERR_INVALID_ARG, "multi-partition graphs are not available in this build");
     bfs_graph_desc d = *desc;
     int64_t n = d.n;
     switch (d.kind) {
@@ -146,17 +145,39 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
     if (n > 0x7fffffffLL) fail(BFS_ERR_CAPACITY, "n = " + std::to_string(n) + " exceeds int32 vertex IDs");
     if (d.opts.reindex_by_degree) fail(BFS_ERR_INVALID_ARG, "reindex_by_degree is not available in this build");
     g = new bfs_graph_s();
-    BFS_CUDA(cudaGetDevice(&g->device));
+    if (comm) {
+        BFS_CUDA(cudaSetDevice(comm->device));
+        g->device = comm->device;
+    } else {
+        BFS_CUDA(cudaGetDevice(&g->device));
+    }
     g->stream = (cudaStream_t)cuda_stream;
     g->n = n;
-    g->lo = 0;
-    g->hi = n;
+    g->comm = comm;
+    if (comm && comm->nranks > 1) {
+        g->nb = part_block(n, comm->nranks);
+        g->lo = std::min<int64_t>(n, (int64_t)comm->rank * g->nb);
+        g->hi = std::min<int64_t>(n, g->lo + g->nb);
+    } else {
+        g->nb = n;
+        g->lo = 0;
+        g->hi = n;
+    }
     g->opts = d.opts;
     cudaEvent_t e0, e1;
     BFS_CUDA(cudaEventCreate(&e0));
     BFS_CUDA(cudaEventCreate(&e1));
     BFS_CUDA(cudaEventRecord(e0, g->stream));
     build_graph(g, &d);
+    if (comm && comm->nranks > 1) {
+        // global arc count for the switch rule (m_u)
+        DevBuf<int64_t> a;
+        a.alloc(1, g->stream);
+        BFS_CUDA(cudaMemcpyAsync(a.p, &g->arcs_local, sizeof(int64_t), cudaMemcpyHostToDevice, g->stream));
+        comm->allreduce_sum_i64(a.p, 1, g->stream);
+        BFS_CUDA(cudaMemcpyAsync(&g->arcs_global, a.p, sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream));
+        BFS_CUDA(cudaStreamSynchronize(g->stream));
+    }
     BFS_CUDA(cudaEventRecord(e1, g->stream));
     BFS_CUDA(cudaEventSynchronize(e1));
     float ms = 0;
@@ -281,26 +302,40 @@ bfs_status bfs_graph_destroy(bfs_graph_t g) {
 }
 
 bfs_status bfs_comm_unique_id(uint8_t id[128]) {
-    (void)id;
-    set_error("multi-GPU communicator is not available in this build");
-    return BFS_ERR_NCCL;
+    API_BEGIN
+    if (!id) fail(BFS_ERR_INVALID_ARG, "id is NULL");
+    comm_unique_id(id);
+    API_END
 }
 
 bfs_status bfs_comm_create(int nranks, int rank, const uint8_t id[128], int device, bfs_comm_t* out) {
-    (void)nranks; (void)rank; (void)id; (void)device; (void)out;
-    set_error("multi-GPU communicator is not available in this build");
-    return BFS_ERR_NCCL;
+    API_BEGIN
+    if (!id || !out) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    *out = comm_create_nccl(nranks, rank, id, device);
+    API_END
 }
 
 bfs_status bfs_comm_create_local(int nparts, int device, bfs_comm_t* out) {
-    (void)nparts; (void)device; (void)out;
-    set_error("local multi-partition communicator is not available in this build");
-    return BFS_ERR_INVALID_ARG;
+    API_BEGIN
+    if (!out) fail(BFS_ERR_INVALID_ARG, "out is NULL");
+    comm_create_local(nparts, device, out);
+    API_END
 }
 
 bfs_status bfs_comm_destroy(bfs_comm_t comm) {
-    (void)comm;
-    return BFS_OK;
+    API_BEGIN
+    delete comm;
+    API_END
+}
+
+bfs_status bfs_partition_range(int64_t n, int nranks, int rank, int64_t* local_begin, int64_t* local_end) {
+    API_BEGIN
+    if (n < 1 || nranks < 1 || rank < 0 || rank >= nranks || !local_begin || !local_end)
+        fail(BFS_ERR_INVALID_ARG, "bad partition arguments");
+    const int64_t nb = nranks > 1 ? part_block(n, nranks) : n;
+    *local_begin = std::min<int64_t>(n, (int64_t)rank * nb);
+    *local_end = std::min<int64_t>(n, *local_begin + nb);
+    API_END
 }
 
 bfs_status bfs_kronecker_edges(const bfs_kron_spec* spec, int64_t first, int64_t count, int32_t* uv_out,

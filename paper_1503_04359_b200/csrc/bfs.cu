@@ -1,31 +1,32 @@
-// The hot path: level-synchronous direction-optimized BFS on one GPU
-// (Alg. 1; Beamer via P:16; switch rule
-// P:151-155 read as DESIGN.md R2/R3/R17/R19).
+// The hot path: level-synchronous direction-optimized BFS (
+// Alg. 1; Beamer via P:16; switch rule P:151-155 read as
+// DESIGN.md R2/R3/R17/R19), on one GPU or 1D-partitioned over p ranks
+// (Alg. 2/3 P:119-140).
 //
-// Data layout in HBM (internal labels, owned range [lo, hi), nl = hi - lo):
-//   off     int64[nl+1]   CSR offsets          adj   int32[arcs] global IDs
+// Data layout in HBM on a rank that owns internal labels [lo, hi), nl = hi - lo:
+//   off     int64[nl+1]   CSR offsets of owned rows    adj int32[arcs] global IDs
 //   visited u32[nl/32]    1 = visited or degree 0 (initialised from the skip mask)
-//   front / next u32[n/32] frontier bitmaps (bottom-up input / output)
-//   q0 / q1 int32[nl]     frontier queues (top-down input / output)
-//   depth / parent int32[nl]  outputs, each entry written exactly once
+//   front / next u32[p*nb/32]  global frontier bitmaps; a rank writes its own slice
+//   q0 / q1 int32[nl]     frontier queues of owned vertices (global IDs)
+//   depth / parent int32[nl]   outputs, each entry written exactly once
+//   (p > 1) seen u32[n/32] remote-claim dedup, out/in int2 claim lists
 //
 // Kernels:
 //   k_init        visited <- skip | root, root outputs, counters
 //   k_td_expand   top-down step, edge-balanced: a device scan of frontier degrees
-//                 gives every CTA a contiguous 2048-arc chunk; arcs are mapped back
-//                 to their frontier vertex by binary search in shared memory;
-//                 unvisited targets are claimed with atomicOr on the visited word;
-//                 winners write depth/parent and append to the next queue with one
-//                 warp-aggregated atomicAdd; m_f of the next frontier is fused.
-//   k_bu_step     bottom-up step, one warp per 32-vertex visited word: lanes scan
-//                 their own row for up to kBuLaneSteps arcs (first frontier
-//                 neighbour wins: `break for`), then rows still unresolved
-//                 are scanned by the whole warp 32 arcs at a time with a ballot
-//                 (lowest lane = first in row order).  n_f, m_f, inspections fused.
-//   k_q2b / k_b2q frontier queue <-> bitmap on direction switches (ballot/popc +
-//                 warp prefix sums, one atomicAdd per warp)
+//                 gives each CTA a contiguous chunk of arcs; arcs map back to their
+//                 frontier vertex by binary search in shared memory; owned targets
+//                 are claimed with atomicOr on the visited word, remote targets are
+//                 deduplicated in `seen` and appended as (v, parent) claims for the
+//                 owner; winners stage the next queue in shared memory (one global
+//                 atomicAdd per CTA chunk); m_f of the next frontier is fused.
+//   k_td_merge    owner side of the push (Alg. 2): claims received from peers
+//   k_bu_batch    bottom-up step: warp per 32-word batch, per-lane rows with
+//                 kBuSlots in flight, warp-cooperative long rows (see below)
+//   k_q2b / k_b2q frontier queue <-> bitmap on direction switches
 //   k_finalize    parent = depth = -1 for unreached vertices (write-once outputs)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
@@ -35,13 +36,11 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTdThreads = 256;
-constexpr int kTdItems = 8;
+constexpr int kTdItems = 4;
 constexpr int kTdChunk = kTdThreads * kTdItems;  // arcs per CTA iteration
-constexpr int kBuThreads = 256;
-constexpr int kBuLaneSteps = 4;
 
-// counter slots
-enum { C_NEXT = 0, C_MF = 1, C_INSP = 2, C_B2Q = 3, C_SCAN = 4, C_TUPLES = 8 };
+// counter slots: [0, 8) written by this rank's kernels, [8, 16) global (allreduced)
+enum { C_NEXT = 0, C_MF = 1, C_INSP = 2, C_B2Q = 3, C_SCAN = 4, C_WORK = 5, C_TUPLES = 6, C_GLOBAL = 8 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
@@ -55,49 +54,73 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
     return x;
 }
 
+// root_l < 0 on ranks that do not own the root
 __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int64_t root_l, int32_t root_g,
                        int32_t* depth, int32_t* parent, int32_t* q, const int64_t* off, unsigned long long* cnt) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
-        if (w == (root_l >> 5)) x |= 1u << (root_l & 31);
+        if (root_l >= 0 && w == (root_l >> 5)) x |= 1u << (root_l & 31);
         visited[w] = x;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        depth[root_l] = 0;
-        parent[root_l] = root_g;
-        q[0] = root_g;
-        cnt[C_NEXT] = 1;
-        cnt[C_MF] = (unsigned long long)(off[root_l + 1] - off[root_l]);
-        cnt[C_INSP] = 0;
+        for (int i = 0; i < 16; ++i) cnt[i] = 0;
+        if (root_l >= 0) {
+            depth[root_l] = 0;
+            parent[root_l] = root_g;
+            q[0] = root_g;
+            cnt[C_NEXT] = 1;
+            cnt[C_MF] = (unsigned long long)(off[root_l + 1] - off[root_l]);
+        }
     }
 }
 
 // chunk c of the top-down arc range starts inside frontier entry starts[c]
 __global__ void k_td_chunk_starts(const int64_t* prefix, int64_t F, int64_t nchunks, int64_t* starts) {
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
-        int64_t e = c * kTdChunk;
+        const int64_t e = c * kTdChunk;
         // largest i in [0, F) with prefix[i] <= e (prefix non-decreasing, prefix[0] = 0)
-        int64_t lo = 0, hi = F - 1;
-        while (lo < hi) {
-            int64_t mid = (lo + hi + 1) >> 1;
-            if (prefix[mid] <= e) lo = mid;
-            else hi = mid - 1;
+        int64_t a = 0, b = F - 1;
+        while (a < b) {
+            const int64_t mid = (a + b + 1) >> 1;
+            if (prefix[mid] <= e) a = mid;
+            else b = mid - 1;
         }
-        starts[c] = lo;
+        starts[c] = a;
     }
 }
 
+struct Remote {          // p > 1 only
+    uint32_t* seen;      // global bitmap: remote vertices this rank already claimed in this BFS
+    int2* out;           // claims (v, parent) for peer q at out[q * cap ...]
+    unsigned long long* out_cnt;  // [p]
+    int64_t cap;
+    int64_t nb;          // partition block size
+};
+
+// Top-down step (Alg. 1 TD branch).  Each CTA iteration handles one chunk of
+// kTdChunk consecutive arcs in three phases so that the dependent loads of the
+// kTdItems arcs of a thread overlap:
+//   A  locate (binary search in shared memory) and load all targets v
+//   B  probe the visited words, then atomicOr-claim the unvisited ones
+//   C  winners write depth/parent and stage v in shared memory; one atomicAdd per
+//      CTA chunk on the global queue tail, then a coalesced copy of the stage.
+template <bool kMulti>
 __global__ void __launch_bounds__(kTdThreads)
 k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
-            int32_t* __restrict__ qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo) {
+            int32_t* __restrict__ qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo,
+            int64_t hi, Remote rm) {
     __shared__ int64_t s_pre[kTdChunk + 2];
     __shared__ int64_t s_beg[kTdChunk + 1];
     __shared__ int32_t s_u[kTdChunk + 1];
+    __shared__ int32_t s_q[kTdChunk];
+    __shared__ int s_qn;
+    __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31;
     unsigned long long my_mf = 0;
     const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
+    if (threadIdx.x == 0) s_qn = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
         const int64_t e0 = c * kTdChunk;
         const int64_t e1 = min(E, e0 + kTdChunk);
@@ -109,62 +132,140 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
             for (int k = threadIdx.x; k <= cntv; k += kTdThreads) {
                 s_pre[k] = prefix[i0 + k];
                 if (k < cntv) {
-                    int32_t u = q[i0 + k];
+                    const int32_t u = q[i0 + k];
                     s_u[k] = u;
                     s_beg[k] = off[u - lo];
                 }
             }
         }
         __syncthreads();
-#pragma unroll 2
+        int32_t v[kTdItems], u[kTdItems];
+        // A: targets
+#pragma unroll
         for (int j = 0; j < kTdItems; ++j) {
             const int64_t e = e0 + (int64_t)j * kTdThreads + threadIdx.x;
-            bool win = false;
-            int32_t v = 0, u = 0;
+            v[j] = -1;
+            u[j] = 0;
             if (e < e1) {
                 int64_t beg, pre;
                 if (fits) {
                     int a = 0, b = (int)cntv - 1;
                     while (a < b) {
-                        int mid = (a + b + 1) >> 1;
+                        const int mid = (a + b + 1) >> 1;
                         if (s_pre[mid] <= e) a = mid;
                         else b = mid - 1;
                     }
-                    u = s_u[a];
+                    u[j] = s_u[a];
                     beg = s_beg[a];
                     pre = s_pre[a];
                 } else {
                     int64_t a = i0, b = F - 1;
                     while (a < b) {
-                        int64_t mid = (a + b + 1) >> 1;
+                        const int64_t mid = (a + b + 1) >> 1;
                         if (prefix[mid] <= e) a = mid;
                         else b = mid - 1;
                     }
-                    u = q[a];
-                    beg = off[u - lo];
+                    u[j] = q[a];
+                    beg = off[u[j] - lo];
                     pre = prefix[a];
                 }
-                v = __ldg(adj + beg + (e - pre));
-                const uint32_t bit = 1u << (v & 31);
-                uint32_t* wp = visited + ((v - lo) >> 5);
-                if (!(__ldcg(wp) & bit)) win = !(atomicOr(wp, bit) & bit);
+                v[j] = __ldg(adj + beg + (e - pre));
             }
-            const unsigned m = __ballot_sync(kFull, win);
+        }
+        // B: probe, then claim.  Owned targets in `visited`, remote ones in `seen`.
+        bool own[kTdItems];
+        uint32_t* wp[kTdItems];
+        uint32_t wv[kTdItems];
+#pragma unroll
+        for (int j = 0; j < kTdItems; ++j) {
+            own[j] = !kMulti || (v[j] >= lo && v[j] < hi);
+            wp[j] = nullptr;
+            if (v[j] >= 0) wp[j] = own[j] ? visited + ((v[j] - lo) >> 5) : rm.seen + (v[j] >> 5);
+            wv[j] = wp[j] ? __ldcg(wp[j]) : kFull;
+        }
+        bool win[kTdItems];
+#pragma unroll
+        for (int j = 0; j < kTdItems; ++j) {
+            const uint32_t bit = 1u << (v[j] & 31);
+            win[j] = false;
+            if (wp[j] && !(wv[j] & bit)) win[j] = !(atomicOr(wp[j], bit) & bit);
+        }
+        // C: outputs + staged queue append; remote claims go to the owner's list
+#pragma unroll
+        for (int j = 0; j < kTdItems; ++j) {
+            const bool lw = win[j] && own[j];
+            const unsigned m = __ballot_sync(kFull, lw);
             if (m) {
                 const int leader = __ffs(m) - 1;
-                unsigned long long base = 0;
-                if (lane == leader) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+                int base = 0;
+                if (lane == leader) base = atomicAdd(&s_qn, __popc(m));
                 base = __shfl_sync(kFull, base, leader);
-                if (win) {
-                    const int64_t vl = v - lo;
-                    qnext[base + __popc(m & lanemask_lt())] = v;
+                if (lw) {
+                    const int64_t vl = v[j] - lo;
+                    s_q[base + __popc(m & lanemask_lt())] = v[j];
                     depth[vl] = next_level;
-                    parent[vl] = u;
+                    parent[vl] = u[j];
                     my_mf += (unsigned long long)(off[vl + 1] - off[vl]);
+                }
+            }
+            if (kMulti) {
+                const bool rw = win[j] && !own[j];
+                if (__ballot_sync(kFull, rw)) {
+                    const int owner = rw ? (int)(v[j] / rm.nb) : -1;
+                    const unsigned peers = __match_any_sync(kFull, owner);
+                    const int leader = __ffs(peers) - 1;
+                    unsigned long long pos = 0;
+                    if (rw && lane == leader) pos = atomicAdd(rm.out_cnt + owner, (unsigned long long)__popc(peers));
+                    pos = __shfl_sync(kFull, pos, leader);
+                    if (rw) rm.out[(int64_t)owner * rm.cap + (int64_t)pos + __popc(peers & lanemask_lt())] = make_int2(v[j], u[j]);
                 }
             }
         }
         __syncthreads();
+        const int qn = s_qn;
+        if (threadIdx.x == 0 && qn) s_base = atomicAdd(cnt + C_NEXT, (unsigned long long)qn);
+        __syncthreads();
+        for (int k = threadIdx.x; k < qn; k += kTdThreads) qnext[s_base + k] = s_q[k];
+        __syncthreads();
+        if (threadIdx.x == 0) s_qn = 0;
+    }
+    my_mf = warp_sum_u64(my_mf);
+    if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+}
+
+// Owner side of the top-down push: claims (v, parent) received from peers are
+// claimed exactly like local top-down targets (Alg. 2 "(local) ==> (remote)").
+__global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t* __restrict__ off,
+                           uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
+                           int32_t* __restrict__ qnext, unsigned long long* __restrict__ cnt, int32_t next_level,
+                           int64_t lo) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long my_mf = 0;
+    for (int64_t b0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; b0 < R;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b0 + lane;
+        bool win = false;
+        int2 c = make_int2(0, 0);
+        if (i < R) {
+            c = in[i];
+            const uint32_t bit = 1u << (c.x & 31);
+            uint32_t* wp = visited + ((c.x - lo) >> 5);
+            if (!(__ldcg(wp) & bit)) win = !(atomicOr(wp, bit) & bit);
+        }
+        const unsigned m = __ballot_sync(kFull, win);
+        if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+            base = __shfl_sync(kFull, base, leader);
+            if (win) {
+                const int64_t vl = c.x - lo;
+                qnext[base + __popc(m & lanemask_lt())] = c.x;
+                depth[vl] = next_level;
+                parent[vl] = c.y;
+                my_mf += (unsigned long long)(off[vl + 1] - off[vl]);
+            }
+        }
     }
     my_mf = warp_sum_u64(my_mf);
     if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
@@ -174,114 +275,211 @@ __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int
     return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
 
-__global__ void __launch_bounds__(kBuThreads)
-k_bu_step(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uint32_t* __restrict__ visited,
-          const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int32_t* __restrict__ depth,
-          int32_t* __restrict__ parent, int64_t words, int64_t lo, int32_t next_level,
-          unsigned long long* __restrict__ cnt) {
-    const int lane = threadIdx.x & 31;
-    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    const int64_t wbase = lo >> 5;  // first global word of the owned range
+// Bottom-up step (Alg. 1 BU branch, `break for` P:107, R1).
+// A warp takes a batch of 32 visited words (1024 owned vertices) at a time from a
+// global work counter:
+//   1. one coalesced 128-byte load of the 32 visited words; an all-visited batch
+//      costs only that load and a coalesced store of 32 zero next-words;
+//   2. the unvisited vertices of the batch are compacted into a per-warp list in
+//      shared memory (popc + warp prefix sum);
+//   3. every lane keeps kBuSlots rows in flight and advances all of them each
+//      round (independent adj[j] loads, then independent frontier-bit probes),
+//      refilling a slot from the list as soon as its row resolves -- this hides
+//      the off -> adj -> frontier dependent-load chain behind kBuSlots-way MLP
+//      (the paper's "virtual warp" of one lane per vertex);
+//   4. a row still unresolved after kBuLong lane-serial probes moves to a per-warp
+//      list and is finished by the whole warp, 32 arcs per ballot (the lowest
+//      hitting lane is the first frontier neighbour in row order);
+//   5. the 32 next words are assembled in shared memory and stored coalesced.
+constexpr int kBuWarps = 8;
+constexpr int kBuSlots = 4;
+constexpr int kBuLong = 8;
+constexpr int kLongCap = 64;
+
+__global__ void __launch_bounds__(kBuWarps * 32)
+k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uint32_t* __restrict__ visited,
+           const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int32_t* __restrict__ depth,
+           int32_t* __restrict__ parent, int64_t words, int64_t lo, int32_t next_level,
+           unsigned long long* __restrict__ cnt) {
+    __shared__ uint16_t s_list[kBuWarps][1024];
+    __shared__ uint32_t s_nb[kBuWarps][32];
+    __shared__ int64_t s_lj[kBuWarps][kLongCap];
+    __shared__ int64_t s_le[kBuWarps][kLongCap];
+    __shared__ int32_t s_lv[kBuWarps][kLongCap];
+    __shared__ int32_t s_ld[kBuWarps][kLongCap];
+    __shared__ int s_lcount[kBuWarps];
+    const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    uint16_t* list = s_list[wid];
+    uint32_t* nbw = s_nb[wid];
+    const int64_t wbase = lo >> 5;
+    const int64_t nbatches = (words + 31) / 32;
     unsigned long long my_nf = 0, my_mf = 0, my_insp = 0, my_scan = 0;
-    for (int64_t w = gw; w < words; w += nw) {
-        const uint32_t vis = visited[w];
-        if (vis == kFull) {
-            if (lane == 0) next[wbase + w] = 0u;
+    for (;;) {
+        long long bt = 0;
+        if (lane == 0) bt = (long long)atomicAdd(cnt + C_WORK, 1ull);
+        bt = __shfl_sync(kFull, bt, 0);
+        if (bt >= nbatches) break;
+        const int64_t w = bt * 32 + lane;
+        const uint32_t vis = w < words ? visited[w] : kFull;
+        const uint32_t un = ~vis;
+        if (!__ballot_sync(kFull, un != 0u)) {
+            if (w < words) next[wbase + w] = 0u;
             continue;
         }
-        const int64_t vl = w * 32 + lane;
-        const bool todo = !((vis >> lane) & 1u);
-        if (lane == 0) my_scan += __popc(~vis);
-        int64_t b = 0, e = 0;
-        if (todo) {
-            b = off[vl];
-            e = off[vl + 1];
-        }
-        int64_t j = b;
-        bool found = false;
-        int32_t par = -1;
-        // phase 1: each lane walks its own row (virtual warp of 1)
+        // 2. compact unvisited local indices (0..1023) into the per-warp list
+        const int c = __popc(un);
+        int inc = c;
 #pragma unroll
-        for (int t = 0; t < kBuLaneSteps; ++t) {
-            if (!found && j < e) {
-                int32_t u = __ldg(adj + j);
-                if (in_front(front, u)) {
-                    found = true;
-                    par = u;
-                } else {
-                    ++j;
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += y;
+        }
+        const int U = __shfl_sync(kFull, inc, 31);
+        {
+            uint32_t bits = un;
+            int p = inc - c;
+            while (bits) {
+                const int k = __ffs(bits) - 1;
+                bits &= bits - 1;
+                list[p++] = (uint16_t)(lane * 32 + k);
+            }
+        }
+        nbw[lane] = 0u;
+        if (lane == 0) s_lcount[wid] = 0;
+        my_scan += (unsigned long long)c;
+        __syncwarp();
+        // 3. lane-serial scan with kBuSlots rows in flight per lane
+        const int64_t vbase = bt * 1024;
+        int t = lane;
+        int32_t sv[kBuSlots], sd[kBuSlots];
+        int64_t sj[kBuSlots], se[kBuSlots];
+        bool sa[kBuSlots];
+#pragma unroll
+        for (int s = 0; s < kBuSlots; ++s) {
+            sa[s] = false;
+            sv[s] = 0;
+            sd[s] = 0;
+            sj[s] = se[s] = 0;
+            if (t < U) {
+                sv[s] = list[t];
+                t += 32;
+                sj[s] = off[vbase + sv[s]];
+                se[s] = off[vbase + sv[s] + 1];
+                sd[s] = (int32_t)(se[s] - sj[s]);
+                sa[s] = sj[s] < se[s];
+            }
+        }
+        for (;;) {
+            bool any = false;
+#pragma unroll
+            for (int s = 0; s < kBuSlots; ++s) any |= sa[s];
+            if (!__any_sync(kFull, any)) break;
+            int32_t u[kBuSlots];
+#pragma unroll
+            for (int s = 0; s < kBuSlots; ++s) u[s] = sa[s] ? __ldg(adj + sj[s]) : 0;
+            bool h[kBuSlots];
+#pragma unroll
+            for (int s = 0; s < kBuSlots; ++s) h[s] = sa[s] && in_front(front, u[s]);
+#pragma unroll
+            for (int s = 0; s < kBuSlots; ++s) {
+                if (sa[s]) {
+                    my_insp += 1;
+                    if (h[s]) {
+                        depth[vbase + sv[s]] = next_level;
+                        parent[vbase + sv[s]] = u[s];
+                        atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
+                        my_mf += (unsigned long long)sd[s];
+                        sa[s] = false;
+                    } else if (++sj[s] == se[s]) {
+                        sa[s] = false;  // exhausted: no frontier neighbour this level
+                    } else if (sd[s] - (se[s] - sj[s]) >= kBuLong) {
+                        const int idx = atomicAdd(s_lcount + wid, 1);
+                        if (idx < kLongCap) {  // hand the rest of the row to the warp
+                            s_lv[wid][idx] = sv[s];
+                            s_lj[wid][idx] = sj[s];
+                            s_le[wid][idx] = se[s];
+                            s_ld[wid][idx] = sd[s];
+                            sa[s] = false;
+                        }
+                    }
+                }
+                if (!sa[s] && t < U) {
+                    sv[s] = list[t];
+                    t += 32;
+                    sj[s] = off[vbase + sv[s]];
+                    se[s] = off[vbase + sv[s] + 1];
+                    sd[s] = (int32_t)(se[s] - sj[s]);
+                    sa[s] = sj[s] < se[s];
                 }
             }
         }
-        // phase 2: unresolved rows, one at a time, scanned by the whole warp
-        unsigned rem = __ballot_sync(kFull, !found && j < e);
-        while (rem) {
-            const int src = __ffs(rem) - 1;
-            rem &= rem - 1;
-            const int64_t jb = __shfl_sync(kFull, j, src);
-            const int64_t je = __shfl_sync(kFull, e, src);
-            int64_t hit_j = je;
-            int32_t hit_u = -1;
+        __syncwarp();
+        // 4. long rows: whole warp, 32 arcs per ballot
+        const int L = min(s_lcount[wid], kLongCap);
+        for (int x = 0; x < L; ++x) {
+            const int32_t lv = s_lv[wid][x];
+            const int64_t jb = s_lj[wid][x], je = s_le[wid][x];
+            int64_t hit = -1;
+            int32_t hu = 0;
             for (int64_t j0 = jb; j0 < je; j0 += 32) {
                 const int64_t jj = j0 + lane;
-                int32_t u = -1;
-                bool h = false;
+                int32_t uu = 0;
+                bool hh = false;
                 if (jj < je) {
-                    u = __ldg(adj + jj);
-                    h = in_front(front, u);
+                    uu = __ldg(adj + jj);
+                    hh = in_front(front, uu);
                 }
-                const unsigned hm = __ballot_sync(kFull, h);
+                const unsigned hm = __ballot_sync(kFull, hh);
                 if (hm) {
                     const int first = __ffs(hm) - 1;
-                    hit_j = j0 + first;
-                    hit_u = __shfl_sync(kFull, u, first);
+                    hit = j0 + first;
+                    hu = __shfl_sync(kFull, uu, first);
                     break;
                 }
             }
-            if (lane == src) {
-                j = hit_j;
-                if (hit_u >= 0) {
-                    found = true;
-                    par = hit_u;
+            if (lane == 0) {
+                if (hit >= 0) {
+                    depth[vbase + lv] = next_level;
+                    parent[vbase + lv] = hu;
+                    nbw[lv >> 5] |= 1u << (lv & 31);
+                    my_mf += (unsigned long long)s_ld[wid][x];
+                    my_insp += (unsigned long long)(hit - jb + 1);
+                } else {
+                    my_insp += (unsigned long long)(je - jb);
                 }
             }
         }
-        if (found) {
-            depth[vl] = next_level;
-            parent[vl] = par;
-        }
-        const unsigned nb = __ballot_sync(kFull, found);
-        if (lane == 0) {
+        __syncwarp();
+        // 5. coalesced next / visited words
+        if (w < words) {
+            const uint32_t nb = nbw[lane];
             next[wbase + w] = nb;
-            visited[w] = vis | nb;
-            my_nf += __popc(nb);
+            if (nb) visited[w] = vis | nb;
+            my_nf += (unsigned long long)__popc(nb);
         }
-        if (todo) {
-            my_insp += (unsigned long long)(found ? (j - b + 1) : (e - b));
-            if (found) my_mf += (unsigned long long)(e - b);
-        }
+        __syncwarp();
     }
     my_nf = warp_sum_u64(my_nf);
     my_mf = warp_sum_u64(my_mf);
     my_insp = warp_sum_u64(my_insp);
-    if (lane == 0 && my_scan) atomicAdd(cnt + C_SCAN, my_scan);
+    my_scan = warp_sum_u64(my_scan);
     if (lane == 0) {
         if (my_nf) atomicAdd(cnt + C_NEXT, my_nf);
         if (my_mf) atomicAdd(cnt + C_MF, my_mf);
         if (my_insp) atomicAdd(cnt + C_INSP, my_insp);
+        if (my_scan) atomicAdd(cnt + C_SCAN, my_scan);
     }
 }
 
-// queue -> bitmap (front cleared beforehand)
+// queue -> bitmap (the owned slice of front is cleared beforehand)
 __global__ void k_q2b(const int32_t* __restrict__ q, int64_t F, uint32_t* __restrict__ front) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F; i += (int64_t)gridDim.x * blockDim.x) {
-        int32_t v = q[i];
+        const int32_t v = q[i];
         atomicOr(front + (v >> 5), 1u << (v & 31));
     }
 }
 
-// bitmap (owned words) -> queue of global IDs
+// owned slice of a bitmap -> queue of global IDs
 __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, int32_t* __restrict__ q,
                       unsigned long long* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
@@ -290,11 +488,11 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
          b0 += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = b0 + lane;
         uint32_t bits = w < words ? bm[wbase + w] : 0u;
-        int c = __popc(bits);
+        const int c = __popc(bits);
         int inc = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
-            int y = __shfl_up_sync(kFull, inc, d);
+            const int y = __shfl_up_sync(kFull, inc, d);
             if (lane >= d) inc += y;
         }
         const int total = __shfl_sync(kFull, inc, 31);
@@ -323,7 +521,7 @@ __global__ void k_finalize(const uint32_t* __restrict__ visited, const uint32_t*
     }
 }
 
-// original-label outputs from internal-label ones (degree reindex)
+// original-label outputs from internal-label ones (degree reindex, one GPU)
 __global__ void k_remap_out(const int32_t* __restrict__ label, const int32_t* __restrict__ ilabel,
                             const int32_t* __restrict__ dep_i, const int32_t* __restrict__ par_i, int64_t n,
                             int32_t* __restrict__ dep_o, int32_t* __restrict__ par_o) {
@@ -351,36 +549,50 @@ __global__ void k_component_degree(const uint32_t* __restrict__ visited, const u
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(out, s);
 }
 
-// non-self-loop arc count of candidate roots (internal labels), one warp per candidate
+// non-self-loop arc count of owned candidate roots (internal labels), one warp per
+// candidate; candidates outside [lo, hi) or negative contribute 0
 __global__ void k_nonloop_degree(const int32_t* __restrict__ cand, int64_t k, const int64_t* __restrict__ off,
-                                 const int32_t* __restrict__ adj, int64_t lo, int64_t* __restrict__ out) {
+                                 const int32_t* __restrict__ adj, int64_t lo, int64_t hi, int64_t* __restrict__ out) {
     const int lane = threadIdx.x & 31;
     const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = gw; t < k; t += nw) {
         const int32_t r = cand[t];
-        const int64_t b = off[r - lo], e = off[r - lo + 1];
         int64_t c = 0;
-        for (int64_t j = b + lane; j < e; j += 32) c += adj[j] != r;
+        if (r >= lo && r < hi) {
+            const int64_t b = off[r - lo], e = off[r - lo + 1];
+            for (int64_t j = b + lane; j < e; j += 32) c += adj[j] != r;
+        }
         for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(kFull, c, d);
         if (lane == 0) out[t] = c;
     }
 }
 
+__global__ void k_gather_labels(const int32_t* __restrict__ label, const int32_t* __restrict__ in, int64_t k,
+                                int32_t* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < k; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in[i] < 0 ? -1 : label[in[i]];
+}
+
 int grid_for(int64_t items, int threads, int per_sm = 8) {
-    int64_t b = (items + threads - 1) / threads;
-    int64_t cap = (int64_t)num_sms() * per_sm;
+    const int64_t b = (items + threads - 1) / threads;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
     return (int)std::max<int64_t>(1, std::min(b, cap));
 }
+
+bool multi(const bfs_graph_s* g) { return g->comm && g->comm->nranks > 1; }
 
 }  // namespace
 
 void bfs_alloc_state(bfs_graph_s* g) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
+    const int p = g->comm ? g->comm->nranks : 1;
     g->visited.alloc((size_t)padded_words(nl), s);
-    g->front.alloc((size_t)padded_words(g->n), s);
-    g->next.alloc((size_t)padded_words(g->n), s);
+    // global bitmaps: p slices of nb/32 words (nb is a multiple of 32)
+    const int64_t gwords = p > 1 ? (int64_t)p * (g->nb / 32) : padded_words(g->n);
+    g->front.alloc((size_t)gwords + 4, s);
+    g->next.alloc((size_t)gwords + 4, s);
     BFS_CUDA(cudaMemsetAsync(g->front.p, 0, g->front.bytes(), s));
     BFS_CUDA(cudaMemsetAsync(g->next.p, 0, g->next.bytes(), s));
     g->q0.alloc((size_t)std::max<int64_t>(nl, 1), s);
@@ -388,14 +600,32 @@ void bfs_alloc_state(bfs_graph_s* g) {
     g->prefix.alloc((size_t)nl + 1, s);
     g->cnt.alloc(16, s);
     g->scratch64.alloc((size_t)(g->arcs_local / kTdChunk + 2), s);  // TD chunk starts
+    if (p > 1) {
+        g->seen.alloc((size_t)padded_words(g->n), s);
+        g->out_cnt.alloc((size_t)p, s);
+        g->cnt_mat.alloc((size_t)p * p, s);
+        if (!g->h_cnt_mat) BFS_CUDA(cudaMallocHost(&g->h_cnt_mat, (size_t)p * p * sizeof(int64_t)));
+    }
     if (!g->h_cnt) BFS_CUDA(cudaMallocHost(&g->h_cnt, 16 * sizeof(int64_t)));
     for (auto& e : g->ev)
         if (!e) BFS_CUDA(cudaEventCreate(&e));
 }
 
-static void read_counters(bfs_graph_s* g) {
-    BFS_CUDA(cudaMemcpyAsync(g->h_cnt, g->cnt.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream));
-    BFS_CUDA(cudaStreamSynchronize(g->stream));
+// local counters [0,8) -> global [8,16) (allreduce on p ranks), then to the host
+static void sync_counters(bfs_graph_s* g) {
+    cudaStream_t s = g->stream;
+    BFS_CUDA(cudaMemcpyAsync(g->cnt.p + C_GLOBAL, g->cnt.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (multi(g)) g->comm->allreduce_sum_i64(g->cnt.p + C_GLOBAL, 8, s);
+    BFS_CUDA(cudaMemcpyAsync(g->h_cnt, g->cnt.p, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaStreamSynchronize(s));
+}
+
+template <class T>
+static void ensure(DevBuf<T>& b, size_t count, cudaStream_t s) {
+    if (b.count < count) {
+        b.reset();
+        b.alloc(std::max(count, b.count * 2), s);
+    }
 }
 
 void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out) {
@@ -403,6 +633,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         fail(BFS_ERR_OUT_OF_RANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g->n) + ")");
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
+    const bool mg = multi(g);
+    const int p = mg ? g->comm->nranks : 1;
+    const int me = mg ? g->comm->rank : 0;
     unsigned long long* cnt = (unsigned long long*)g->cnt.p;
     int64_t* h = g->h_cnt;
 
@@ -412,9 +645,10 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         BFS_CUDA(cudaMemcpy(&r, g->label.p + root, sizeof(int32_t), cudaMemcpyDeviceToHost));
         root_i = r;
     }
-    const int64_t root_l = root_i - g->lo;
+    const bool own_root = root_i >= g->lo && root_i < g->hi;
+    const int64_t root_l = own_root ? root_i - g->lo : -1;
 
-    // where the kernels write (internal order)
+    // where the kernels write (internal order, owned slice)
     const bool dev_depth = depth_out && is_device_ptr(depth_out);
     const bool dev_parent = parent_out && is_device_ptr(parent_out);
     int32_t* kd = (!g->reindexed && dev_depth) ? depth_out : nullptr;
@@ -432,11 +666,12 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     g->run = bfs_run_stats{};
     g->run.root = root;
     int64_t launches = 0;
-    // per-step events: [3d] step start, [3d+1] main kernel start, [3d+2] main kernel end
+    // per-step events: [4d] step start, [4d+1] main kernel start, [4d+2] main kernel end,
+    // [4d+3] exchange end (p > 1)
     const bool lt = g->policy.level_times != 0;
     constexpr int kMaxTimed = 64;
     if (lt && g->lev_ev.empty()) {
-        g->lev_ev.resize(3 * kMaxTimed + 1);
+        g->lev_ev.resize(4 * kMaxTimed + 1);
         for (auto& e : g->lev_ev) BFS_CUDA(cudaEventCreate(&e));
     }
 
@@ -446,7 +681,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                                              g->off.p, cnt);
     BFS_CHECK_LAUNCH();
     ++launches;
-    read_counters(g);
+    if (mg) BFS_CUDA(cudaMemsetAsync(g->seen.p, 0, g->seen.bytes(), s));
+    sync_counters(g);
+    BFS_CUDA(cudaEventRecord(g->ev[2], s));  // end of init
 
     int32_t* qcur = g->q0.p;
     int32_t* qnxt = g->q1.p;
@@ -454,8 +691,15 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     uint32_t* next = g->next.p;
     bool have_queue = true;
     int dir = 0;  // 0 TD, 1 BU
-    int64_t n_f = h[C_NEXT], m_f = h[C_MF], prev_nf = 0, seen = 0, reached = 0;
+    int64_t n_f = h[C_GLOBAL + C_NEXT], m_f = h[C_GLOBAL + C_MF];
+    int64_t nf_loc = h[C_NEXT], mf_loc = h[C_MF];
+    int64_t prev_nf = 0, seen = 0, reached = 0;
     const int64_t words = words_of(nl);
+    const size_t slice_bytes = mg ? (size_t)(g->nb / 8) : 0;
+    uint64_t nvl_total = 0;
+    std::vector<size_t> sendb(p), recvb(p);
+    std::vector<const void*> sendp(p);
+    std::vector<void*> recvp(p);
     for (int d = 0; n_f > 0; ++d) {
         if (d >= (1 << 30)) fail(BFS_ERR_INTERNAL, "level loop did not terminate");
         reached += n_f;
@@ -473,79 +717,135 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 }
         }
         const bool timed = lt && d < kMaxTimed;
-        if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d], s));
+        if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d], s));
         BFS_CUDA(cudaMemsetAsync(g->cnt.p, 0, 8 * sizeof(int64_t), s));
-        int64_t insp, scanned;
+        int64_t insp = -1, scanned = -1;
+        uint64_t nvl = 0;
         if (dir == 0) {
+            // ---------------- top-down (Alg. 1, push Alg. 2)
             if (!have_queue) {
                 k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, qcur, cnt);
                 BFS_CHECK_LAUNCH();
                 ++launches;
                 have_queue = true;
             }
-            const int64_t E = m_f;
+            const int64_t E = mf_loc;
+            Remote rm{};
+            if (mg) {
+                rm.nb = g->nb;
+                rm.cap = std::max<int64_t>(1, std::min<int64_t>(g->nb, E));
+                ensure(g->out_list, (size_t)(p * rm.cap), s);
+                rm.seen = g->seen.p;
+                rm.out = g->out_list.p;
+                rm.out_cnt = (unsigned long long*)g->out_cnt.p;
+                BFS_CUDA(cudaMemsetAsync(g->out_cnt.p, 0, (size_t)p * sizeof(int64_t), s));
+            }
+            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             if (E > 0) {
-                launches += scan_queue_degrees(qcur, n_f, g->off.p, g->lo, g->prefix.p, s);
+                launches += scan_queue_degrees(qcur, nf_loc, g->off.p, g->lo, g->prefix.p, s);
                 const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
-                k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, n_f, nchunks, g->scratch64.p);
+                k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p);
                 BFS_CHECK_LAUNCH();
-                if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 1], s));
-                k_td_expand<<<grid_for(nchunks * kTdThreads, kTdThreads, 8), kTdThreads, 0, s>>>(
-                    qcur, g->prefix.p, g->scratch64.p, n_f, E, g->off.p, g->adj.p, g->visited.p, kd, kp, qnxt, cnt,
-                    d + 1, g->lo);
+                const int grid = grid_for(nchunks * kTdThreads, kTdThreads, 8);
+                if (mg)
+                    k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
+                                                                  g->adj.p, g->visited.p, kd, kp, qnxt, cnt, d + 1,
+                                                                  g->lo, g->hi, rm);
+                else
+                    k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
+                                                                   g->off.p, g->adj.p, g->visited.p, kd, kp, qnxt, cnt,
+                                                                   d + 1, g->lo, g->hi, rm);
                 BFS_CHECK_LAUNCH();
-                if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 2], s));
                 launches += 2;
-            } else if (timed) {
-                BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 1], s));
-                BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 2], s));
+            }
+            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
+            if (mg) {
+                // push: counts matrix (allgather), then claims to their owners (alltoallv)
+                BFS_CUDA(cudaMemcpyAsync(g->cnt_mat.p + (size_t)me * p, g->out_cnt.p, (size_t)p * 8,
+                                         cudaMemcpyDeviceToDevice, s));
+                g->comm->allgather_inplace(g->cnt_mat.p, (size_t)p * 8, s);
+                BFS_CUDA(cudaMemcpyAsync(g->h_cnt_mat, g->cnt_mat.p, (size_t)p * p * 8, cudaMemcpyDeviceToHost, s));
+                BFS_CUDA(cudaStreamSynchronize(s));
+                int64_t R = 0;
+                for (int q = 0; q < p; ++q) R += q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
+                ensure(g->in_list, (size_t)std::max<int64_t>(R, 1), s);
+                int64_t roff = 0;
+                for (int q = 0; q < p; ++q) {
+                    const int64_t out_q = q == me ? 0 : g->h_cnt_mat[(size_t)me * p + q];
+                    const int64_t in_q = q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
+                    sendp[q] = g->out_list.p + (size_t)q * rm.cap;
+                    sendb[q] = (size_t)out_q * sizeof(int2);
+                    recvp[q] = g->in_list.p + roff;
+                    recvb[q] = (size_t)in_q * sizeof(int2);
+                    roff += in_q;
+                    nvl += sendb[q];
+                }
+                g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
+                if (R > 0) {
+                    k_td_merge<<<grid_for(R, 256), 256, 0, s>>>(g->in_list.p, R, g->off.p, g->visited.p, kd, kp, qnxt,
+                                                                cnt, d + 1, g->lo);
+                    BFS_CHECK_LAUNCH();
+                    ++launches;
+                }
             }
             std::swap(qcur, qnxt);
             insp = E;
-            scanned = n_f;
+            scanned = nf_loc;
         } else {
+            // ---------------- bottom-up (Alg. 1, pull Alg. 3)
             if (have_queue) {
-                BFS_CUDA(cudaMemsetAsync(front, 0, g->front.bytes(), s));
-                k_q2b<<<grid_for(n_f, 256), 256, 0, s>>>(qcur, n_f, front);
-                BFS_CHECK_LAUNCH();
-                ++launches;
+                BFS_CUDA(cudaMemsetAsync(front + (g->lo >> 5), 0, (size_t)words_of(nl) * 4, s));
+                if (nf_loc) {
+                    k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur, nf_loc, front);
+                    BFS_CHECK_LAUNCH();
+                    ++launches;
+                }
                 have_queue = false;
             }
-            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 1], s));
-            k_bu_step<<<grid_for(words * 32, kBuThreads, 8), kBuThreads, 0, s>>>(
+            if (mg) {
+                g->comm->allgather_inplace(front, slice_bytes, s);
+                nvl = slice_bytes * (size_t)(p - 1);
+            }
+            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
+            const int64_t nbatches = (words + 31) / 32;
+            k_bu_batch<<<grid_for(nbatches * 32, kBuWarps * 32, 8), kBuWarps * 32, 0, s>>>(
                 g->off.p, g->adj.p, g->visited.p, front, next, kd, kp, words, g->lo, d + 1, cnt);
             BFS_CHECK_LAUNCH();
-            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * d + 2], s));
+            if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;
             std::swap(front, next);
-            insp = -1;
-            scanned = -1;
         }
-        read_counters(g);
+        if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 3], s));
+        sync_counters(g);
         bfs_level_stats L{};
         L.level = d;
         L.direction = dir;
         L.frontier = n_f;
-        L.discovered = h[C_NEXT];
+        L.discovered = h[C_GLOBAL + C_NEXT];
         L.m_f = m_f;
         L.m_u = m_u;
-        L.inspections = insp >= 0 ? insp : h[C_INSP];
-        L.scanned = scanned >= 0 ? scanned : h[C_SCAN];
+        L.inspections = dir == 0 ? m_f : h[C_GLOBAL + C_INSP];
+        L.scanned = dir == 0 ? n_f : h[C_GLOBAL + C_SCAN];
+        L.nvlink_bytes = nvl;
+        (void)insp;
+        (void)scanned;
+        nvl_total += nvl;
         g->levels.push_back(L);
         prev_nf = n_f;
-        n_f = h[C_NEXT];
-        m_f = h[C_MF];
+        n_f = h[C_GLOBAL + C_NEXT];
+        m_f = h[C_GLOBAL + C_MF];
+        nf_loc = h[C_NEXT];
+        mf_loc = h[C_MF];
     }
     const int ntimed = lt ? (int)std::min<size_t>(g->levels.size(), kMaxTimed) : 0;
-    if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[3 * ntimed], s));
+    if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
     k_finalize<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, nl, root_l, kd, kp);
     BFS_CHECK_LAUNCH();
     ++launches;
     if (g->reindexed) {
         int32_t* od = dev_depth ? depth_out : nullptr;
         int32_t* op = dev_parent ? parent_out : nullptr;
-        // host outputs: remap into staging buffers, then copy
-        DevBuf<int32_t> hd, hp;
+        DevBuf<int32_t> hd, hp;  // host outputs: remap into staging buffers, then copy
         if (depth_out && !dev_depth) { hd.alloc((size_t)nl, s); od = hd.p; }
         if (parent_out && !dev_parent) { hp.alloc((size_t)nl, s); op = hp.p; }
         k_remap_out<<<grid_for(g->n, 256), 256, 0, s>>>(g->label.p, g->ilabel.p, kd, kp, g->n, od, op);
@@ -561,20 +861,37 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         if (parent_out && !dev_parent) BFS_CUDA(cudaMemcpyAsync(parent_out, kp, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
         BFS_CUDA(cudaStreamSynchronize(s));
     }
-    float ms = 0;
+    float ms = 0, ms_init = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
+    BFS_CUDA(cudaEventElapsedTime(&ms_init, g->ev[0], g->ev[2]));
     g->run.ms_total = ms;
-    g->run.ms_compute = ms;
+    g->run.ms_init = ms_init;
     g->run.levels = (int)g->levels.size();
     g->run.reached = reached;
     g->run.kernel_launches = launches;
+    g->run.nvlink_bytes = nvl_total;
+    double push = 0, pull = 0, comp = 0;
     for (int d = 0; d < ntimed; ++d) {
-        float x = 0, k = 0;
-        BFS_CUDA(cudaEventElapsedTime(&x, g->lev_ev[3 * d], g->lev_ev[3 * d + 3]));
-        BFS_CUDA(cudaEventElapsedTime(&k, g->lev_ev[3 * d + 1], g->lev_ev[3 * d + 2]));
+        float x = 0, k = 0, xe = 0;
+        BFS_CUDA(cudaEventElapsedTime(&x, g->lev_ev[4 * d], g->lev_ev[4 * d + 4]));
+        BFS_CUDA(cudaEventElapsedTime(&k, g->lev_ev[4 * d + 1], g->lev_ev[4 * d + 2]));
+        BFS_CUDA(cudaEventElapsedTime(&xe, g->lev_ev[4 * d + 2], g->lev_ev[4 * d + 3]));
         g->levels[d].ms = x;
         g->levels[d].kernel_ms = k;
+        comp += k;
+        if (mg) {
+            if (g->levels[d].direction == 0) {
+                push += xe;
+            } else {
+                float pre = 0;
+                BFS_CUDA(cudaEventElapsedTime(&pre, g->lev_ev[4 * d], g->lev_ev[4 * d + 1]));
+                pull += pre;
+            }
+        }
     }
+    g->run.ms_compute = lt ? comp : ms - ms_init;
+    g->run.ms_push = push;
+    g->run.ms_pull = pull;
     g->last_root_l = root_l;
     g->run.component_edge_tuples = -1;  // computed lazily by bfs_stats
 }
@@ -585,6 +902,7 @@ int64_t component_tuples_impl(bfs_graph_s* g) {
     k_component_degree<<<grid_for(g->nl(), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->deg_raw.p, g->nl(),
                                                               g->last_root_l, (unsigned long long*)g->cnt.p + C_TUPLES);
     BFS_CHECK_LAUNCH();
+    if (multi(g)) g->comm->allreduce_sum_i64(g->cnt.p + C_TUPLES, 1, s);
     int64_t v = 0;
     BFS_CUDA(cudaMemcpyAsync(&v, g->cnt.p + C_TUPLES, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFS_CUDA(cudaStreamSynchronize(s));
@@ -597,11 +915,11 @@ void sample_roots_impl(bfs_graph_s* g, uint32_t scale, uint64_t seed, int64_t co
     const int64_t max_cand = 64 * count + 4 * g->n;
     const int64_t B = 4096;
     std::vector<int32_t> cand;
-    std::vector<int32_t> cand_i;
     std::vector<int64_t> deg(B);
-    DevBuf<int32_t> dcand;
+    DevBuf<int32_t> dcand, dint;
     DevBuf<int64_t> ddeg;
     dcand.alloc(B, s);
+    dint.alloc(B, s);
     ddeg.alloc(B, s);
     int64_t got = 0;
     for (int64_t k0 = 0; k0 < max_cand && got < count; k0 += B) {
@@ -609,27 +927,23 @@ void sample_roots_impl(bfs_graph_s* g, uint32_t scale, uint64_t seed, int64_t co
         for (int64_t k = k0; k < std::min(max_cand, k0 + B); ++k) {
             uint32_t ctr[4] = {(uint32_t)((uint64_t)k & 0xffffffffu), (uint32_t)((uint64_t)k >> 32), 0u, 2u}, w[4];
             philox4x32_10_host(ctr, key, w);
-            int64_t r = scale == 0 ? 0 : (int64_t)(w[0] >> (32 - scale));
+            const int64_t r = scale == 0 ? 0 : (int64_t)(w[0] >> (32 - scale));
             cand.push_back(r < g->n ? (int32_t)r : -1);
         }
-        // map to internal labels, count non-self-loop arcs on the device
-        std::vector<int32_t> valid;
-        for (int32_t r : cand) valid.push_back(r < 0 ? 0 : r);
-        BFS_CUDA(cudaMemcpyAsync(dcand.p, valid.data(), valid.size() * 4, cudaMemcpyHostToDevice, s));
+        const int64_t K = (int64_t)cand.size();
+        BFS_CUDA(cudaMemcpyAsync(dcand.p, cand.data(), (size_t)K * 4, cudaMemcpyHostToDevice, s));
+        const int32_t* di = dcand.p;
         if (g->reindexed) {
-            // gather label[cand] in place via a tiny copy (host loop is fine: B small)
-            cand_i.resize(valid.size());
-            for (size_t t = 0; t < valid.size(); ++t)
-                BFS_CUDA(cudaMemcpyAsync(&cand_i[t], g->label.p + valid[t], 4, cudaMemcpyDeviceToHost, s));
-            BFS_CUDA(cudaStreamSynchronize(s));
-            BFS_CUDA(cudaMemcpyAsync(dcand.p, cand_i.data(), cand_i.size() * 4, cudaMemcpyHostToDevice, s));
+            k_gather_labels<<<grid_for(K, 256), 256, 0, s>>>(g->label.p, dcand.p, K, dint.p);
+            BFS_CHECK_LAUNCH();
+            di = dint.p;
         }
-        k_nonloop_degree<<<grid_for((int64_t)valid.size() * 32, 256), 256, 0, s>>>(dcand.p, (int64_t)valid.size(),
-                                                                                 g->off.p, g->adj.p, g->lo, ddeg.p);
+        k_nonloop_degree<<<grid_for(K * 32, 256), 256, 0, s>>>(di, K, g->off.p, g->adj.p, g->lo, g->hi, ddeg.p);
         BFS_CHECK_LAUNCH();
-        BFS_CUDA(cudaMemcpyAsync(deg.data(), ddeg.p, valid.size() * 8, cudaMemcpyDeviceToHost, s));
+        if (multi(g)) g->comm->allreduce_sum_i64(ddeg.p, (int)K, s);
+        BFS_CUDA(cudaMemcpyAsync(deg.data(), ddeg.p, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
         BFS_CUDA(cudaStreamSynchronize(s));
-        for (size_t t = 0; t < cand.size() && got < count; ++t) {
+        for (int64_t t = 0; t < K && got < count; ++t) {
             if (cand[t] < 0 || deg[t] == 0) continue;
             bool dup = false;
             for (int64_t x = 0; x < got; ++x)

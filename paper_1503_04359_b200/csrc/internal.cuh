@@ -89,9 +89,30 @@ int scan_exclusive_i32(const int32_t* in, int64_t* out, int64_t n, cudaStream_t 
 int scan_queue_degrees(const int32_t* q, int64_t F, const int64_t* off, int64_t lo, int64_t* out,
                         cudaStream_t s);
 
-// ---------------------------------------------------------------- communication (comm.cu)
-struct Comm;  // NCCL-backed or local-simulated; defined in comm.cu
+}  // namespace bfsb
 
+// ---------------------------------------------------------------- communication (comm.cu)
+// The opaque bfs_comm_t of the C ABI: one rank's endpoint.  Backends: NCCL (one
+// process per GPU) and local (p host threads of one process on one device).
+struct bfs_comm_s {
+    int nranks = 1, rank = 0, device = 0;
+    virtual ~bfs_comm_s() = default;
+    // buf holds nranks slices of bytes_per_rank; slice `rank` is the input, all slices the output
+    virtual void allgather_inplace(void* buf, size_t bytes_per_rank, cudaStream_t s) = 0;
+    virtual void allreduce_sum_i64(int64_t* buf, int count, cudaStream_t s) = 0;
+    virtual void allreduce_max_i64(int64_t* buf, int count, cudaStream_t s) = 0;
+    // variable-size all-to-all; entries for q == rank are ignored
+    virtual void alltoallv(const void* const* sendp, const size_t* sendb, void* const* recvp, const size_t* recvb,
+                           cudaStream_t s) = 0;
+};
+
+namespace bfsb {
+using Comm = bfs_comm_s;
+void comm_unique_id(uint8_t id[128]);
+Comm* comm_create_nccl(int nranks, int rank, const uint8_t id[128], int device);
+void comm_create_local(int nparts, int device, Comm** out);
+// 1D block partition: every rank owns a word-aligned contiguous range
+inline int64_t part_block(int64_t n, int p) { return ((n + p - 1) / p + 31) / 32 * 32; }
 }  // namespace bfsb
 
 // ---------------------------------------------------------------- the handle
@@ -128,7 +149,14 @@ struct bfs_graph_s {
     bfsb::DevBuf<int64_t> cnt;       // [8] device counters
     int64_t* h_cnt = nullptr;        // pinned mirror
     bfsb::DevBuf<int32_t> tmp_depth, tmp_parent;  // internal-label outputs / host staging
-    bfsb::DevBuf<int64_t> scratch64; // small reductions
+    bfsb::DevBuf<int64_t> scratch64; // TD chunk starts
+    // 1D partition (p > 1)
+    int64_t nb = 0;                  // block size: rank r owns [r*nb, min(n, (r+1)*nb))
+    bfsb::DevBuf<uint32_t> seen;     // [n/32] remote vertices already claimed this BFS
+    bfsb::DevBuf<int2> out_list, in_list;  // (vertex, parent) claims
+    bfsb::DevBuf<int64_t> out_cnt;   // [p]
+    bfsb::DevBuf<int64_t> cnt_mat;   // [p*p] claim counts, row = sender
+    int64_t* h_cnt_mat = nullptr;    // pinned mirror
 
     bfs_policy policy{0, 15, 18, 0, 0};
     std::vector<bfs_level_stats> levels;

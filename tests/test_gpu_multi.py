@@ -1,0 +1,136 @@
+"""Multi-partition parity on one GPU: p rank endpoints of a local communicator,
+each driven from its own host thread through the same C ABI calls, kernels and
+host logic as the one-process-per-GPU NCCL path (only the transport differs).
+The concatenated owned slices must match the oracle exactly as on one GPU, and
+the global per-step counters must equal the emulator's on every rank."""
+import numpy as np
+import pytest
+
+import oracle
+from tests import graphs
+
+torch = pytest.importorskip("torch")
+pkg = pytest.importorskip("paper_1503_04359_b200")
+from paper_1503_04359_b200 import build as pkg_build  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _dev():
+    pkg_build.build()
+    torch.cuda.set_device(0)
+
+
+def _build(p, make):
+    comms = pkg.bfs_comm_create_local(p, 0)
+
+    def mk(r):
+        torch.cuda.set_device(0)
+        s = torch.cuda.Stream()
+        return make(comms[r], s)
+
+    gs = pkg.run_ranks(mk, p)
+    return comms, gs
+
+
+def _run_all(gs, root, policy):
+    p = len(gs)
+
+    def go(r):
+        torch.cuda.set_device(0)
+        g = gs[r]
+        g.set_policy(**policy)
+        with torch.cuda.stream(g.stream):
+            parent, depth = g.run(int(root))
+        g.stream.synchronize()
+        run, levels = g.stats()
+        return parent.cpu().numpy(), depth.cpu().numpy(), run, levels
+
+    res = pkg.run_ranks(go, p)
+    parent = np.concatenate([x[0] for x in res])
+    depth = np.concatenate([x[1] for x in res])
+    return parent, depth, [x[2] for x in res], [x[3] for x in res]
+
+
+def _check(gs, ref, root, policy, uv=None):
+    parent, depth, runs, levels = _run_all(gs, root, policy)
+    want, _ = oracle.bfs(ref, int(root))
+    assert np.array_equal(depth, want), np.nonzero(depth != want)[0][:10]
+    assert not oracle.validate(ref, int(root), depth, parent, ref_depth=want)
+    emu = oracle.do_emulate(ref, want, alpha=policy.get("alpha", 15), beta=policy.get("beta", 18),
+                            policy=policy.get("mode", 0), bu_from=policy.get("bu_from_level", 0),
+                            want_bu_parent=True)
+    for lv in levels:   # every rank reports the same global counters
+        for key, lk in (("dir", "direction"), ("n_f", "frontier"), ("discovered", "discovered"),
+                        ("m_f", "m_f"), ("m_u", "m_u"), ("insp", "inspections")):
+            assert [x[lk] for x in lv] == emu[key].tolist(), key
+    bu = emu["bu_parent"] >= 0
+    assert np.array_equal(parent[bu], emu["bu_parent"][bu])
+    for run in runs:
+        assert run["reached"] == int((want >= 0).sum())
+        if uv is not None:
+            assert run["component_edge_tuples"] == oracle.component_tuples(uv, want)
+    return runs, levels
+
+
+def _close(comms, gs):
+    for g in gs:
+        g.close()
+    for c in comms:
+        pkg.bfs_comm_destroy(c)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+def test_partition_ranges_tile(p):
+    n = 1000
+    rs = [pkg.bfs_partition_range(n, p, r) for r in range(p)]
+    assert rs[0][0] == 0 and rs[-1][1] == n
+    for (a, b), (c, d) in zip(rs, rs[1:]):
+        assert b == c and a % 32 == 0
+
+
+def test_g1_two_partitions():
+    """push OR-merges claims into the owner; pull overwrites frontier views."""
+    n, uv = graphs.g1()
+    ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    comms, gs = _build(2, lambda c, s: pkg.Graph.from_edges(uv, n, comm=c, stream=s))
+    for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
+        for root in range(n):
+            _check(gs, ref, root, pol, uv)
+    _close(comms, gs)
+
+
+@pytest.mark.parametrize("p", [2, 3, 4, 8])
+@pytest.mark.parametrize("abc", [oracle.KRON_ABC, oracle.ER_ABC])
+def test_kronecker_s14(p, abc):
+    scale, seed = 14, 7
+    uv, ref = oracle.kron_graph(scale, 16, seed, abc)
+    comms, gs = _build(p, lambda c, s: pkg.Graph.kronecker(scale, 16, seed, abc, comm=c, stream=s))
+    # every rank holds exactly the oracle rows of its range
+    for g in gs:
+        off, adj = g.export_csr()
+        lo, hi = g.local_begin, g.local_end
+        assert np.array_equal(off.cpu().numpy(), ref.offsets[lo:hi + 1] - ref.offsets[lo])
+        assert np.array_equal(adj.cpu().numpy(), ref.adj[ref.offsets[lo]:ref.offsets[hi]])
+    roots = pkg.run_ranks(lambda r: gs[r].sample_roots(scale, seed, 6), p)
+    assert all(np.array_equal(roots[0], x) for x in roots)
+    assert np.array_equal(roots[0], oracle.sample_roots(ref, scale, seed, 6))
+    pols = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=0, alpha=2, beta=4)]
+    for i, r in enumerate(roots[0]):
+        runs, levels = _check(gs, ref, r, pols[i % len(pols)], uv)
+        if p > 1:
+            assert sum(x["nvlink_bytes"] for x in levels[0]) == runs[0]["nvlink_bytes"]
+    _close(comms, gs)
+
+
+@pytest.mark.parametrize("p", [2, 5])
+def test_fixtures_multi(p):
+    for name, (n, uv) in {"union": graphs.disjoint_union(graphs.path(40), graphs.star(90), graphs.clique(9)),
+                          "skewed": graphs.skewed_edges(4000, 30000, 5), "grid": graphs.grid(20, 31)}.items():
+        ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+        comms, gs = _build(p, lambda c, s: pkg.Graph.from_edges(uv, n, comm=c, stream=s))
+        for root in sorted({0, n - 1, int(np.argmax(ref.degree()))}):
+            for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
+                _check(gs, ref, root, pol, uv)
+        _close(comms, gs)

@@ -1,0 +1,32 @@
+"""Small driver for ncu captures: build one config's graph, run R roots.
+
+    ncu ... python tools/profile_run.py --config k26 --roots 2
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+import paper_1503_04359_b200 as pkg  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="k26")
+ap.add_argument("--roots", type=int, default=2)
+ap.add_argument("--skip", type=int, default=0, help="roots to skip (sampled order)")
+ap.add_argument("--mode", type=int, default=0)
+a = ap.parse_args()
+cfg = bench.CONFIGS[a.config]
+torch.cuda.set_device(0)
+g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"])
+roots = g.sample_roots(cfg["scale"], cfg["seed"], a.skip + a.roots)[a.skip:]
+g.set_policy(mode=a.mode, level_times=True)
+for r in roots:
+    p, d = g.run(int(r))
+    run, levels = g.stats()
+    print(int(r), round(run["ms_total"], 4), [(lv["direction"], lv["frontier"], round(lv["kernel_ms"], 4)) for lv in levels])
+torch.cuda.synchronize()
