@@ -212,6 +212,7 @@ def main():
     ap.add_argument("--alpha", type=int, default=15)
     ap.add_argument("--beta", type=int, default=18)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--reindex", type=int, default=0, help="section 3.4 degree reindex (P:158)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--levels-out", default=None, help="write per-level records (JSON) here")
     args = ap.parse_args()
@@ -246,7 +247,8 @@ def main():
 
     cfg = CONFIGS[args.config]
     stream = torch.cuda.Stream()
-    g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], comm=comm, stream=stream)
+    opts = pkg.default_opts(reindex_by_degree=bool(args.reindex))
+    g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], opts=opts, comm=comm, stream=stream)
     build_ms = g.build_ms
     roots = g.sample_roots(cfg["scale"], cfg["seed"], args.roots)
     n = g.n
@@ -351,6 +353,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": cfg["name"], "scale": cfg["scale"], "edgefactor": cfg["ef"], "seed": cfg["seed"],
                    "roots": len(roots), "alpha": args.alpha, "beta": args.beta, "parallelism": f"1d{ws}",
+                   "reindex_by_degree": bool(args.reindex),
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((8 * (n + 1) + 4 * g.arcs) / 1e9)},
         "build_ms": round(build_ms, 2), "arcs": g.arcs,
         "per_root_ms": {"min": round(min(times), 4), "median": round(statistics.median(times), 4),

@@ -54,9 +54,24 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
     return x;
 }
 
+// A top-down frontier queue: vertex (global ID) plus its row begin and degree,
+// recorded when the vertex is discovered (its offsets are read then anyway) so
+// that expanding it never re-reads `off` at random.
+struct Queue {
+    int32_t* v;
+    int64_t* beg;
+    int32_t* deg;
+};
+
+__device__ __forceinline__ void queue_put(const Queue& q, unsigned long long pos, int32_t v, int64_t beg, int32_t deg) {
+    q.v[pos] = v;
+    q.beg[pos] = beg;
+    q.deg[pos] = deg;
+}
+
 // root_l < 0 on ranks that do not own the root
 __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int64_t root_l, int32_t root_g,
-                       int32_t* depth, int32_t* parent, int32_t* q, const int64_t* off, unsigned long long* cnt) {
+                       int32_t* depth, int32_t* parent, Queue q, const int64_t* off, unsigned long long* cnt) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
         if (root_l >= 0 && w == (root_l >> 5)) x |= 1u << (root_l & 31);
@@ -67,9 +82,10 @@ __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int6
         if (root_l >= 0) {
             depth[root_l] = 0;
             parent[root_l] = root_g;
-            q[0] = root_g;
+            const int64_t b = off[root_l], e = off[root_l + 1];
+            queue_put(q, 0, root_g, b, (int32_t)(e - b));
             cnt[C_NEXT] = 1;
-            cnt[C_MF] = (unsigned long long)(off[root_l + 1] - off[root_l]);
+            cnt[C_MF] = (unsigned long long)(e - b);
         }
     }
 }
@@ -106,15 +122,17 @@ struct Remote {          // p > 1 only
 //      CTA chunk on the global queue tail, then a coalesced copy of the stage.
 template <bool kMulti>
 __global__ void __launch_bounds__(kTdThreads)
-k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
+k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
-            int32_t* __restrict__ qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo,
+            const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo,
             int64_t hi, Remote rm) {
     __shared__ int64_t s_pre[kTdChunk + 2];
     __shared__ int64_t s_beg[kTdChunk + 1];
     __shared__ int32_t s_u[kTdChunk + 1];
     __shared__ int32_t s_q[kTdChunk];
+    __shared__ int64_t s_qb[kTdChunk];
+    __shared__ int32_t s_qd[kTdChunk];
     __shared__ int s_qn;
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31;
@@ -132,9 +150,8 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
             for (int k = threadIdx.x; k <= cntv; k += kTdThreads) {
                 s_pre[k] = prefix[i0 + k];
                 if (k < cntv) {
-                    const int32_t u = q[i0 + k];
-                    s_u[k] = u;
-                    s_beg[k] = off[u - lo];
+                    s_u[k] = q.v[i0 + k];
+                    s_beg[k] = q.beg[i0 + k];
                 }
             }
         }
@@ -165,8 +182,8 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
                         if (prefix[mid] <= e) a = mid;
                         else b = mid - 1;
                     }
-                    u[j] = q[a];
-                    beg = off[u[j] - lo];
+                    u[j] = q.v[a];
+                    beg = q.beg[a];
                     pre = prefix[a];
                 }
                 v[j] = __ldg(adj + beg + (e - pre));
@@ -202,10 +219,14 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
                 base = __shfl_sync(kFull, base, leader);
                 if (lw) {
                     const int64_t vl = v[j] - lo;
-                    s_q[base + __popc(m & lanemask_lt())] = v[j];
+                    const int slot = base + __popc(m & lanemask_lt());
+                    const int64_t b = off[vl], e = off[vl + 1];
+                    s_q[slot] = v[j];
+                    s_qb[slot] = b;
+                    s_qd[slot] = (int32_t)(e - b);
                     depth[vl] = next_level;
                     parent[vl] = u[j];
-                    my_mf += (unsigned long long)(off[vl + 1] - off[vl]);
+                    my_mf += (unsigned long long)(e - b);
                 }
             }
             if (kMulti) {
@@ -225,7 +246,7 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
         const int qn = s_qn;
         if (threadIdx.x == 0 && qn) s_base = atomicAdd(cnt + C_NEXT, (unsigned long long)qn);
         __syncthreads();
-        for (int k = threadIdx.x; k < qn; k += kTdThreads) qnext[s_base + k] = s_q[k];
+        for (int k = threadIdx.x; k < qn; k += kTdThreads) queue_put(qnext, s_base + k, s_q[k], s_qb[k], s_qd[k]);
         __syncthreads();
         if (threadIdx.x == 0) s_qn = 0;
     }
@@ -237,7 +258,7 @@ k_td_expand(const int32_t* __restrict__ q, const int64_t* __restrict__ prefix, c
 // claimed exactly like local top-down targets (Alg. 2 "(local) ==> (remote)").
 __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t* __restrict__ off,
                            uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
-                           int32_t* __restrict__ qnext, unsigned long long* __restrict__ cnt, int32_t next_level,
+                           const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level,
                            int64_t lo) {
     const int lane = threadIdx.x & 31;
     unsigned long long my_mf = 0;
@@ -260,10 +281,11 @@ __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t
             base = __shfl_sync(kFull, base, leader);
             if (win) {
                 const int64_t vl = c.x - lo;
-                qnext[base + __popc(m & lanemask_lt())] = c.x;
+                const int64_t b = off[vl], e = off[vl + 1];
+                queue_put(qnext, base + __popc(m & lanemask_lt()), c.x, b, (int32_t)(e - b));
                 depth[vl] = next_level;
                 parent[vl] = c.y;
-                my_mf += (unsigned long long)(off[vl + 1] - off[vl]);
+                my_mf += (unsigned long long)(e - b);
             }
         }
     }
@@ -479,9 +501,9 @@ __global__ void k_q2b(const int32_t* __restrict__ q, int64_t F, uint32_t* __rest
     }
 }
 
-// owned slice of a bitmap -> queue of global IDs
-__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, int32_t* __restrict__ q,
-                      unsigned long long* __restrict__ cnt) {
+// owned slice of a bitmap -> queue of global IDs (with row begin / degree)
+__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, const int64_t* __restrict__ off,
+                      const Queue q, unsigned long long* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int64_t wbase = lo >> 5;
     for (int64_t b0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; b0 < words;
@@ -503,7 +525,9 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
         while (bits) {
             const int k = __ffs(bits) - 1;
             bits &= bits - 1;
-            q[pos++] = (int32_t)(lo + w * 32 + k);
+            const int64_t vl = w * 32 + k;
+            const int64_t b = off[vl], e = off[vl + 1];
+            queue_put(q, pos++, (int32_t)(lo + vl), b, (int32_t)(e - b));
         }
     }
 }
@@ -595,8 +619,13 @@ void bfs_alloc_state(bfs_graph_s* g) {
     g->next.alloc((size_t)gwords + 4, s);
     BFS_CUDA(cudaMemsetAsync(g->front.p, 0, g->front.bytes(), s));
     BFS_CUDA(cudaMemsetAsync(g->next.p, 0, g->next.bytes(), s));
-    g->q0.alloc((size_t)std::max<int64_t>(nl, 1), s);
-    g->q1.alloc((size_t)std::max<int64_t>(nl, 1), s);
+    const size_t qcap = (size_t)std::max<int64_t>(nl, 1);
+    g->q0.alloc(qcap, s);
+    g->q1.alloc(qcap, s);
+    g->qb0.alloc(qcap, s);
+    g->qb1.alloc(qcap, s);
+    g->qd0.alloc(qcap, s);
+    g->qd1.alloc(qcap, s);
     g->prefix.alloc((size_t)nl + 1, s);
     g->cnt.alloc(16, s);
     g->scratch64.alloc((size_t)(g->arcs_local / kTdChunk + 2), s);  // TD chunk starts
@@ -677,7 +706,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
 
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
     const int64_t pw = padded_words(nl);
-    k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, kd, kp, g->q0.p,
+    Queue qcur{g->q0.p, g->qb0.p, g->qd0.p};
+    Queue qnxt{g->q1.p, g->qb1.p, g->qd1.p};
+    k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, kd, kp, qcur,
                                              g->off.p, cnt);
     BFS_CHECK_LAUNCH();
     ++launches;
@@ -685,8 +716,6 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     sync_counters(g);
     BFS_CUDA(cudaEventRecord(g->ev[2], s));  // end of init
 
-    int32_t* qcur = g->q0.p;
-    int32_t* qnxt = g->q1.p;
     uint32_t* front = g->front.p;
     uint32_t* next = g->next.p;
     bool have_queue = true;
@@ -724,7 +753,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         if (dir == 0) {
             // ---------------- top-down (Alg. 1, push Alg. 2)
             if (!have_queue) {
-                k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, qcur, cnt);
+                k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, g->off.p, qcur, cnt);
                 BFS_CHECK_LAUNCH();
                 ++launches;
                 have_queue = true;
@@ -742,7 +771,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             if (E > 0) {
-                launches += scan_queue_degrees(qcur, nf_loc, g->off.p, g->lo, g->prefix.p, s);
+                launches += scan_exclusive_i32(qcur.deg, g->prefix.p, nf_loc, s);
                 const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
                 k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p);
                 BFS_CHECK_LAUNCH();
@@ -796,7 +825,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             if (have_queue) {
                 BFS_CUDA(cudaMemsetAsync(front + (g->lo >> 5), 0, (size_t)words_of(nl) * 4, s));
                 if (nf_loc) {
-                    k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur, nf_loc, front);
+                    k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur.v, nf_loc, front);
                     BFS_CHECK_LAUNCH();
                     ++launches;
                 }

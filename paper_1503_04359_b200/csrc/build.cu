@@ -105,19 +105,57 @@ __global__ void k_kron_edges(KronParams P, uint64_t first, uint64_t count, int2*
     }
 }
 
-// ---- edge sources: generated (Kronecker) or an explicit tuple array
+// ---- edge sources: generated (Kronecker) or an explicit tuple array; with a
+// label array both endpoints are relabeled (second pass of the degree reindex)
 struct KronSource {
     KronParams P;
-    __device__ void get(uint64_t i, uint32_t& u, uint32_t& v) const { kron_edge(P, i, u, v); }
+    const int32_t* label;
+    __device__ void get(uint64_t i, uint32_t& u, uint32_t& v) const {
+        kron_edge(P, i, u, v);
+        if (label) {
+            u = (uint32_t)label[u];
+            v = (uint32_t)label[v];
+        }
+    }
 };
 struct ArraySource {
     const int2* uv;
+    const int32_t* label;
     __device__ void get(uint64_t i, uint32_t& u, uint32_t& v) const {
         int2 t = uv[i];
         u = (uint32_t)t.x;
         v = (uint32_t)t.y;
+        if (label) {
+            u = (uint32_t)label[u];
+            v = (uint32_t)label[v];
+        }
     }
 };
+
+// reindex helpers: key = maxdeg - deg (ascending key = descending degree)
+__global__ void k_degree_max(const int64_t* off, int64_t n, unsigned int* mx) {
+    unsigned int m = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+        m = max(m, (unsigned int)(off[v + 1] - off[v]));
+    for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
+    if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
+}
+
+__global__ void k_degree_keys(const int64_t* off, int64_t n, unsigned int mx, uint32_t* keys, int32_t* vals) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        keys[v] = mx - (unsigned int)(off[v + 1] - off[v]);
+        vals[v] = (int32_t)v;
+    }
+}
+
+// position k -> vertex order[k]: internal label of order[k] is k (one partition)
+__global__ void k_labels(const int32_t* order, int64_t n, int32_t* label, int32_t* ilabel) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[k];
+        label[v] = (int32_t)k;
+        ilabel[k] = v;
+    }
+}
 
 // N1: raw arc count of owned endpoints (a self-loop counts 2)
 template <class Src>
@@ -488,7 +526,7 @@ static void sort_and_compact(bfs_graph_s* g) {
     }
 }
 
-void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
+static void build_pass(bfs_graph_s* g, const bfs_graph_desc* d, const int32_t* label) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
     DevBuf<unsigned int> deg;
@@ -503,7 +541,7 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         P = make_params(&d->kron);
         m = P.m;
         g->tuples = (int64_t)m;
-        k_count<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(KronSource{P}, m, lo, hi, deg.p);
+        k_count<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(KronSource{P, label}, m, lo, hi, deg.p);
         BFS_CHECK_LAUNCH();
     } else if (d->kind == BFS_SRC_EDGES) {
         m = (uint64_t)d->m;
@@ -528,7 +566,7 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
                                               std::to_string(g->n) + ")");
         }
         if (m) {
-            k_count<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(ArraySource{uv_dev.p}, m, lo, hi, deg.p);
+            k_count<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(ArraySource{uv_dev.p, label}, m, lo, hi, deg.p);
             BFS_CHECK_LAUNCH();
         }
     }
@@ -584,9 +622,9 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         cursor.alloc((size_t)nl + 1, s);
         BFS_CUDA(cudaMemcpyAsync(cursor.p, g->off.p, ((size_t)nl + 1) * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
         if (d->kind == BFS_SRC_KRONECKER)
-            k_fill<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(KronSource{P}, m, lo, hi, cursor.p, g->adj.p);
+            k_fill<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(KronSource{P, label}, m, lo, hi, cursor.p, g->adj.p);
         else if (m)
-            k_fill<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(ArraySource{uv_dev.p}, m, lo, hi, cursor.p, g->adj.p);
+            k_fill<<<grid_for((int64_t)m, 256, 16), 256, 0, s>>>(ArraySource{uv_dev.p, label}, m, lo, hi, cursor.p, g->adj.p);
         BFS_CHECK_LAUNCH();
         cursor.reset();
         uv_dev.reset();
@@ -605,6 +643,53 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaStreamSynchronize(s));
     g->arcs_global = g->arcs_local;
+}
+
+// Section 3.4 degree reindex ("reorder vertices in memory to improve local
+// partition access locality" and adjacency lists "in decreasing order of vertex
+// connectivity").  Pass 1 builds the CSR in original labels to get the
+// final (deduplicated) degrees; a stable radix sort orders vertices by (degree
+// desc, ID asc); the position becomes the internal label; pass 2 regenerates the
+// graph with relabeled endpoints, so ascending internal IDs in a row are exactly
+// "decreasing connectivity, ties by original ID".  Isolated vertices end up
+// contiguous at the top of the label range, hubs at the bottom.
+void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
+    if (!d->opts.reindex_by_degree) {
+        build_pass(g, d, nullptr);
+        return;
+    }
+    cudaStream_t s = g->stream;
+    const int64_t n = g->n;
+    build_pass(g, d, nullptr);
+    DevBuf<unsigned int> mx;
+    mx.alloc(1, s);
+    BFS_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned int), s));
+    k_degree_max<<<grid_for(n, 256), 256, 0, s>>>(g->off.p, n, mx.p);
+    BFS_CHECK_LAUNCH();
+    unsigned int hmx = 0;
+    BFS_CUDA(cudaMemcpyAsync(&hmx, mx.p, sizeof(hmx), cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaStreamSynchronize(s));
+    DevBuf<uint32_t> keys;
+    DevBuf<int32_t> order;
+    keys.alloc((size_t)n, s);
+    order.alloc((size_t)n, s);
+    k_degree_keys<<<grid_for(n, 256), 256, 0, s>>>(g->off.p, n, hmx, keys.p, order.p);
+    BFS_CHECK_LAUNCH();
+    // pass-1 graph is no longer needed
+    g->adj.reset();
+    g->off.reset();
+    g->deg_raw.reset();
+    g->skip.reset();
+    const int bits = hmx ? 32 - __builtin_clz(hmx) : 0;
+    radix_sort_pairs(keys.p, order.p, n, bits, s);
+    keys.reset();
+    g->label.alloc((size_t)n, s);
+    g->ilabel.alloc((size_t)n, s);
+    k_labels<<<grid_for(n, 256), 256, 0, s>>>(order.p, n, g->label.p, g->ilabel.p);
+    BFS_CHECK_LAUNCH();
+    order.reset();
+    build_pass(g, d, g->label.p);
+    g->reindexed = true;
 }
 
 }  // namespace bfsb

@@ -145,6 +145,8 @@ struct bfs_graph_s {
     bfsb::DevBuf<uint32_t> front;    // [padded words of n] global frontier bitmap
     bfsb::DevBuf<uint32_t> next;     // [padded words of n] global next bitmap
     bfsb::DevBuf<int32_t> q0, q1;    // [nl] frontier queues (global internal IDs)
+    bfsb::DevBuf<int64_t> qb0, qb1;  // [nl] row begin of each queued vertex
+    bfsb::DevBuf<int32_t> qd0, qd1;  // [nl] degree of each queued vertex
     bfsb::DevBuf<int64_t> prefix;    // [nl + 1] TD degree prefix
     bfsb::DevBuf<int64_t> cnt;       // [8] device counters
     int64_t* h_cnt = nullptr;        // pinned mirror
@@ -172,6 +174,8 @@ struct bfs_graph_s {
 namespace bfsb {
 // build.cu
 void build_graph(bfs_graph_s* g, const bfs_graph_desc* d);
+// sort.cu: stable ascending sort of (key, value) pairs in place
+void radix_sort_pairs(uint32_t* keys, int32_t* vals, int64_t n, int key_bits, cudaStream_t s);
 void kron_edges_device(const bfs_kron_spec* spec, int64_t first, int64_t count, int32_t* uv, cudaStream_t s);
 void validate_kron_spec(const bfs_kron_spec* spec);
 // bfs.cu
