@@ -155,6 +155,17 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
         BFS_CUDA(cudaGetDevice(&g->device));
     }
     g->stream = (cudaStream_t)cuda_stream;
+    {
+        // keep freed blocks in the stream-ordered pool: construction and the TD scans
+        // free and re-allocate GiB-sized temporaries, and returning them to the
+        // driver at every synchronisation costs far more than the kernels
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
     g->n = n;
     g->comm = comm;
     if (comm && comm->nranks > 1) {
@@ -190,6 +201,13 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
     cudaEventDestroy(e1);
     bfs_alloc_state(g);
     BFS_CUDA(cudaStreamSynchronize(g->stream));
+    {
+        // hand construction temporaries back to the driver (the caller's allocator
+        // may need the memory); run-time temporaries stay pooled
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, g->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+        cudaGetLastError();
+    }
     *out = g;
     g = nullptr;
     }

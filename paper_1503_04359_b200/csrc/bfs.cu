@@ -319,7 +319,8 @@ constexpr int kBuLong = 8;
 constexpr int kLongCap = 64;
 
 __global__ void __launch_bounds__(kBuWarps * 32)
-k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uint32_t* __restrict__ visited,
+k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
+           uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int32_t* __restrict__ depth,
            int32_t* __restrict__ parent, int64_t words, int64_t lo, int32_t next_level,
            unsigned long long* __restrict__ cnt) {
@@ -370,25 +371,27 @@ k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uin
         if (lane == 0) s_lcount[wid] = 0;
         my_scan += (unsigned long long)c;
         __syncwarp();
-        // 3. lane-serial scan with kBuSlots rows in flight per lane
+        // 3. lane-serial scan with kBuSlots rows in flight per lane.  A row starts
+        //    "fresh": its first neighbour comes from the dense head record, so the
+        //    common first-probe hit never touches off[] or adj[]; only on a miss is
+        //    off[v] loaded and the rest of the row walked in adj[].
         const int64_t vbase = bt * 1024;
         int t = lane;
-        int32_t sv[kBuSlots], sd[kBuSlots];
+        int32_t sv[kBuSlots], sd[kBuSlots], su[kBuSlots];
         int64_t sj[kBuSlots], se[kBuSlots];
-        bool sa[kBuSlots];
+        bool sa[kBuSlots], sf[kBuSlots];
 #pragma unroll
         for (int s = 0; s < kBuSlots; ++s) {
-            sa[s] = false;
-            sv[s] = 0;
-            sd[s] = 0;
+            sa[s] = sf[s] = false;
+            sv[s] = sd[s] = su[s] = 0;
             sj[s] = se[s] = 0;
             if (t < U) {
                 sv[s] = list[t];
                 t += 32;
-                sj[s] = off[vbase + sv[s]];
-                se[s] = off[vbase + sv[s] + 1];
-                sd[s] = (int32_t)(se[s] - sj[s]);
-                sa[s] = sj[s] < se[s];
+                const int2 hd = __ldg(head + vbase + sv[s]);
+                su[s] = hd.x;
+                sd[s] = hd.y;
+                sa[s] = sf[s] = hd.y > 0;
             }
         }
         for (;;) {
@@ -398,7 +401,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uin
             if (!__any_sync(kFull, any)) break;
             int32_t u[kBuSlots];
 #pragma unroll
-            for (int s = 0; s < kBuSlots; ++s) u[s] = sa[s] ? __ldg(adj + sj[s]) : 0;
+            for (int s = 0; s < kBuSlots; ++s) u[s] = !sa[s] ? 0 : (sf[s] ? su[s] : __ldg(adj + sj[s]));
             bool h[kBuSlots];
 #pragma unroll
             for (int s = 0; s < kBuSlots; ++s) h[s] = sa[s] && in_front(front, u[s]);
@@ -412,6 +415,15 @@ k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uin
                         atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
                         my_mf += (unsigned long long)sd[s];
                         sa[s] = false;
+                    } else if (sf[s]) {
+                        sf[s] = false;
+                        if (sd[s] == 1) {
+                            sa[s] = false;  // single neighbour, not in the frontier
+                        } else {
+                            const int64_t b = off[vbase + sv[s]];
+                            sj[s] = b + 1;
+                            se[s] = b + sd[s];
+                        }
                     } else if (++sj[s] == se[s]) {
                         sa[s] = false;  // exhausted: no frontier neighbour this level
                     } else if (sd[s] - (se[s] - sj[s]) >= kBuLong) {
@@ -428,10 +440,10 @@ k_bu_batch(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, uin
                 if (!sa[s] && t < U) {
                     sv[s] = list[t];
                     t += 32;
-                    sj[s] = off[vbase + sv[s]];
-                    se[s] = off[vbase + sv[s] + 1];
-                    sd[s] = (int32_t)(se[s] - sj[s]);
-                    sa[s] = sj[s] < se[s];
+                    const int2 hd = __ldg(head + vbase + sv[s]);
+                    su[s] = hd.x;
+                    sd[s] = hd.y;
+                    sa[s] = sf[s] = hd.y > 0;
                 }
             }
         }
@@ -838,7 +850,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             const int64_t nbatches = (words + 31) / 32;
             k_bu_batch<<<grid_for(nbatches * 32, kBuWarps * 32, 8), kBuWarps * 32, 0, s>>>(
-                g->off.p, g->adj.p, g->visited.p, front, next, kd, kp, words, g->lo, d + 1, cnt);
+                g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, kd, kp, words, g->lo, d + 1, cnt);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;

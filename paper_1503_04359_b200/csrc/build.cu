@@ -13,11 +13,28 @@
 //   len > 32768    one CTA per row: 32768-element chunks sorted in shared memory,
 //                  then merge-path passes ping-ponging with a scratch buffer.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "internal.cuh"
 
 namespace bfsb {
+
+// BFS_VERBOSE=1 prints wall-clock construction phases (synchronising at each mark)
+struct PhaseLog {
+    bool on = getenv("BFS_VERBOSE") != nullptr;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* what, cudaStream_t s) {
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        auto now = std::chrono::steady_clock::now();
+        fprintf(stderr, "[bfs build] %-24s %9.2f ms\n", what,
+                std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
 
 // ============================================================== Philox4x32-10
 // (Salmon et al. SC'11).  Product-side implementation; the oracle has its own.
@@ -131,6 +148,17 @@ struct ArraySource {
         }
     }
 };
+
+// head[v] = (first neighbour in row order or -1, degree): with rows in canonical
+// order most bottom-up searches end at the first neighbour, so a dense
+// coalesced 8-byte record per vertex replaces the offsets pair + a random
+// adjacency sector on that path.
+__global__ void k_head(const int64_t* off, const int32_t* adj, int64_t nl, int2* head) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = off[v], e = off[v + 1];
+        head[v] = make_int2(e > b ? adj[b] : -1, (int)(e - b));
+    }
+}
 
 // reindex helpers: key = maxdeg - deg (ascending key = descending degree)
 __global__ void k_degree_max(const int64_t* off, int64_t n, unsigned int* mx) {
@@ -529,6 +557,8 @@ static void sort_and_compact(bfs_graph_s* g) {
 static void build_pass(bfs_graph_s* g, const bfs_graph_desc* d, const int32_t* label) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
+    PhaseLog log;
+    log.mark("start", s);
     DevBuf<unsigned int> deg;
     deg.alloc((size_t)std::max<int64_t>(nl, 1), s);
     BFS_CUDA(cudaMemsetAsync(deg.p, 0, deg.bytes(), s));
@@ -629,19 +659,25 @@ static void build_pass(bfs_graph_s* g, const bfs_graph_desc* d, const int32_t* l
         cursor.reset();
         uv_dev.reset();
     }
+    log.mark("count+scan+fill", s);
     // raw degree (TEPS numerator) is what the count pass produced
     g->deg_raw.alloc((size_t)std::max<int64_t>(nl, 1), s);
     BFS_CUDA(cudaMemcpyAsync(g->deg_raw.p, deg.p, (size_t)nl * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     deg.reset();
 
     sort_and_compact(g);
+    log.mark("sort+compact", s);
 
     // degree-0 skip bitmap
     int64_t pw = padded_words(nl);
     g->skip.alloc((size_t)pw, s);
     k_skip_bits<<<grid_for(pw, 256), 256, 0, s>>>(g->off.p, nl, pw, g->skip.p);
     BFS_CHECK_LAUNCH();
+    g->head.alloc((size_t)std::max<int64_t>(nl, 1), s);
+    k_head<<<grid_for(nl, 256), 256, 0, s>>>(g->off.p, g->adj.p, nl, g->head.p);
+    BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaStreamSynchronize(s));
+    log.mark("skip+head", s);
     g->arcs_global = g->arcs_local;
 }
 
@@ -680,6 +716,7 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
     g->off.reset();
     g->deg_raw.reset();
     g->skip.reset();
+    g->head.reset();
     const int bits = hmx ? 32 - __builtin_clz(hmx) : 0;
     radix_sort_pairs(keys.p, order.p, n, bits, s);
     keys.reset();

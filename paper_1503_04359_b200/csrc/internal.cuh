@@ -135,6 +135,7 @@ struct bfs_graph_s {
     bfsb::DevBuf<int32_t> adj;      // [arcs_local]
     bfsb::DevBuf<int32_t> deg_raw;  // [nl] raw arcs per vertex (TEPS numerator)
     bfsb::DevBuf<uint32_t> skip;    // [padded words of nl] bit set = CSR degree 0
+    bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path
     // reindex (identity when absent)
     bool reindexed = false;
     bfsb::DevBuf<int32_t> label;    // [n] original -> internal

@@ -19,10 +19,13 @@ ap.add_argument("--config", default="k26")
 ap.add_argument("--roots", type=int, default=2)
 ap.add_argument("--skip", type=int, default=0, help="roots to skip (sampled order)")
 ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--reindex", type=int, default=0)
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)
-g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"])
+g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"],
+                        opts=pkg.default_opts(reindex_by_degree=bool(a.reindex)))
+print("build_ms", g.build_ms, flush=True)
 roots = g.sample_roots(cfg["scale"], cfg["seed"], a.skip + a.roots)[a.skip:]
 g.set_policy(mode=a.mode, level_times=True)
 for r in roots:
