@@ -38,7 +38,7 @@ CONFIGS = {
     "k29": dict(scale=29, ef=16, seed=1, abc=KRON, name="Graph500 Kronecker scale 29, edgefactor 16"),
     "k30": dict(scale=30, ef=16, seed=1, abc=KRON, name="Graph500 Kronecker scale 30, edgefactor 16"),
 }
-DEFAULT_CONFIG = "k26"
+DEFAULT_CONFIG = "k29"
 METRIC = "Graph500 harmonic-mean GTEPS (64 roots)"
 ROOTS = 64
 # cpu_baseline / reference arm sample: the oracle cannot build s26+ within the bench budget
@@ -209,10 +209,14 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--roots", type=int, default=ROOTS)
-    ap.add_argument("--alpha", type=int, default=15)
-    ap.add_argument("--beta", type=int, default=18)
+    # alpha/beta: the paper gives no values (R2); 30/24 is the B200 sweep optimum
+    # (profiles/r01_switch_sweep.txt); the parity tests cover 15/18 and other settings
+    ap.add_argument("--alpha", type=int, default=30)
+    ap.add_argument("--beta", type=int, default=24)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reindex", type=int, default=0, help="section 3.4 degree reindex (P:158)")
+    ap.add_argument("--rows", default="degree", choices=["id", "degree"],
+                    help="row order: ascending ID (sort_rows 1) or decreasing neighbour degree (2, P:158)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--levels-out", default=None, help="write per-level records (JSON) here")
     args = ap.parse_args()
@@ -247,7 +251,7 @@ def main():
 
     cfg = CONFIGS[args.config]
     stream = torch.cuda.Stream()
-    opts = pkg.default_opts(reindex_by_degree=bool(args.reindex))
+    opts = pkg.default_opts(reindex_by_degree=bool(args.reindex), sort_rows=2 if args.rows == "degree" else 1)
     g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], opts=opts, comm=comm, stream=stream)
     build_ms = g.build_ms
     roots = g.sample_roots(cfg["scale"], cfg["seed"], args.roots)
@@ -353,7 +357,7 @@ def main():
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": cfg["name"], "scale": cfg["scale"], "edgefactor": cfg["ef"], "seed": cfg["seed"],
                    "roots": len(roots), "alpha": args.alpha, "beta": args.beta, "parallelism": f"1d{ws}",
-                   "reindex_by_degree": bool(args.reindex),
+                   "reindex_by_degree": bool(args.reindex), "row_order": args.rows,
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((8 * (n + 1) + 4 * g.arcs) / 1e9)},
         "build_ms": round(build_ms, 2), "arcs": g.arcs,
         "per_root_ms": {"min": round(min(times), 4), "median": round(statistics.median(times), 4),

@@ -14,6 +14,7 @@ Functions and the passage each follows:
 * ``kron_edges``              -- Graph500 Kronecker generator
 * ``build_csr``               -- CSR, each undirected edge as two arcs
 * ``degree_reindex`` / ``relabel_csr`` -- section 3.4 locality reindex
+* ``sort_rows_by_degree``     -- section 3.4 row order without relabeling
 * ``bfs``                     -- serial FIFO BFS, the plain definition
 * ``validate``                -- Graph500 validator V1-V6
 * ``do_emulate``              -- direction rule, counters, inspections
@@ -68,6 +69,7 @@ def _L():
             lib.orc_degree_reindex.argtypes = [i64, P, i64, P, P]
             lib.orc_degree_reindex.restype = i32
             lib.orc_relabel_csr.argtypes = [i64, P, P, P, P, P, P]
+            lib.orc_sort_rows_by_degree.argtypes = [i64, P, P]
             lib.orc_bfs.argtypes = [i64, P, P, i64, P, P]
             lib.orc_bfs.restype = i64
             lib.orc_validate.argtypes = [i64, P, P, i64, P, P, P, P, P]
@@ -180,6 +182,14 @@ def relabel_csr(g: CSR, new_label: np.ndarray, position: np.ndarray) -> CSR:
     pos = _c(position, np.int64)
     _L().orc_relabel_csr(g.n, _p(g.offsets), _p(g.adj), _p(nl), _p(pos), _p(offsets), _p(adj))
     return CSR(g.n, offsets, adj[: g.arcs].copy())
+
+
+def sort_rows_by_degree(g: CSR) -> CSR:
+    """Rows by decreasing neighbour degree, ties by ascending ID; labels unchanged."""
+    adj = g.adj.copy()
+    if g.arcs:
+        _L().orc_sort_rows_by_degree(g.n, _p(g.offsets), _p(adj))
+    return CSR(g.n, g.offsets.copy(), adj)
 
 
 # --------------------------------------------------------------------------- BFS / validation

@@ -261,6 +261,23 @@ void orc_relabel_csr(int64_t n, const int64_t* offsets, const int32_t* adj, cons
     free(inv);
 }
 
+/* Rows in "decreasing order of vertex connectivity, so that the highest degree
+ * vertex in the adjacency list comes first", ties by ascending ID,
+ * labels unchanged: every row of (offsets, adj) is re-sorted in place. */
+static const int64_t* g_row_off;
+static int cmp_nbr_deg_desc(const void* x, const void* y) {
+    int32_t a = *(const int32_t*)x, b = *(const int32_t*)y;
+    int64_t da = g_row_off[a + 1] - g_row_off[a], db = g_row_off[b + 1] - g_row_off[b];
+    if (da != db) return da > db ? -1 : 1;
+    return (a > b) - (a < b);
+}
+
+void orc_sort_rows_by_degree(int64_t n, const int64_t* offsets, int32_t* adj) {
+    g_row_off = offsets;
+    for (int64_t v = 0; v < n; ++v)
+        qsort(adj + offsets[v], (size_t)(offsets[v + 1] - offsets[v]), sizeof(int32_t), cmp_nbr_deg_desc);
+}
+
 /* ------------------------------------------------------------------------- */
 /* Serial FIFO BFS -- the plain definition of BFS depth (section 2.2;
  * S:353-361).  depth[root]=0, parent[root]=root; pop u; for v in adj(u) in

@@ -146,7 +146,8 @@ def _stream_ptr(stream) -> int | None:
     return getattr(stream, "cuda_stream", stream)
 
 
-def default_opts(dedup=True, drop_self_loops=True, reindex_by_degree=False, sort_rows=True) -> bfs_build_opts:
+def default_opts(dedup=True, drop_self_loops=True, reindex_by_degree=False, sort_rows=1) -> bfs_build_opts:
+    """sort_rows: 0 fill order, 1 ascending neighbour ID, 2 decreasing neighbour degree."""
     return bfs_build_opts(int(dedup), int(drop_self_loops), int(reindex_by_degree), int(sort_rows))
 
 

@@ -160,29 +160,37 @@ __global__ void k_head(const int64_t* off, const int32_t* adj, int64_t nl, int2*
     }
 }
 
-// reindex helpers: key = maxdeg - deg (ascending key = descending degree)
-__global__ void k_degree_max(const int64_t* off, int64_t n, unsigned int* mx) {
+// degree-order helpers: key = maxdeg - deg (ascending key = descending degree)
+__global__ void k_local_degree(const int64_t* off, int64_t nl, int32_t* deg) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x)
+        deg[v] = (int32_t)(off[v + 1] - off[v]);
+}
+
+__global__ void k_degree_max(const int32_t* deg, int64_t n, unsigned int* mx) {
     unsigned int m = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
-        m = max(m, (unsigned int)(off[v + 1] - off[v]));
+        m = max(m, (unsigned int)deg[v]);
     for (int d = 16; d > 0; d >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, d));
     if ((threadIdx.x & 31) == 0) atomicMax(mx, m);
 }
 
-__global__ void k_degree_keys(const int64_t* off, int64_t n, unsigned int mx, uint32_t* keys, int32_t* vals) {
+__global__ void k_degree_keys(const int32_t* deg, int64_t n, unsigned int mx, uint32_t* keys, int32_t* vals) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        keys[v] = mx - (unsigned int)(off[v + 1] - off[v]);
+        keys[v] = mx - (unsigned int)deg[v];
         vals[v] = (int32_t)v;
     }
 }
 
-// position k -> vertex order[k]: internal label of order[k] is k (one partition)
-__global__ void k_labels(const int32_t* order, int64_t n, int32_t* label, int32_t* ilabel) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = order[k];
-        label[v] = (int32_t)k;
-        ilabel[k] = v;
-    }
+// order[k] = vertex at position k  ->  rank[vertex] = k
+__global__ void k_rank_of(const int32_t* order, int64_t n, int32_t* rank) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        rank[order[k]] = (int32_t)k;
+}
+
+// adj[j] <- map[adj[j]]
+__global__ void k_map_ids(int32_t* adj, int64_t arcs, const int32_t* map) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < arcs; j += (int64_t)gridDim.x * blockDim.x)
+        adj[j] = map[adj[j]];
 }
 
 // N1: raw arc count of owned endpoints (a self-loop counts 2)
@@ -668,16 +676,7 @@ static void build_pass(bfs_graph_s* g, const bfs_graph_desc* d, const int32_t* l
     sort_and_compact(g);
     log.mark("sort+compact", s);
 
-    // degree-0 skip bitmap
-    int64_t pw = padded_words(nl);
-    g->skip.alloc((size_t)pw, s);
-    k_skip_bits<<<grid_for(pw, 256), 256, 0, s>>>(g->off.p, nl, pw, g->skip.p);
-    BFS_CHECK_LAUNCH();
-    g->head.alloc((size_t)std::max<int64_t>(nl, 1), s);
-    k_head<<<grid_for(nl, 256), 256, 0, s>>>(g->off.p, g->adj.p, nl, g->head.p);
-    BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaStreamSynchronize(s));
-    log.mark("skip+head", s);
     g->arcs_global = g->arcs_local;
 }
 
@@ -689,44 +688,86 @@ static void build_pass(bfs_graph_s* g, const bfs_graph_desc* d, const int32_t* l
 // graph with relabeled endpoints, so ascending internal IDs in a row are exactly
 // "decreasing connectivity, ties by original ID".  Isolated vertices end up
 // contiguous at the top of the label range, hubs at the bottom.
-void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
-    if (!d->opts.reindex_by_degree) {
-        build_pass(g, d, nullptr);
-        return;
-    }
+// Position of every vertex in the (degree desc, ID asc) order of the CURRENT
+// graph: rank[v] = position, order[position] = v.  On p ranks the owned degree
+// slices are allgathered first, so every rank computes the same order.
+static void degree_order(bfs_graph_s* g, DevBuf<int32_t>& rank, DevBuf<int32_t>& order) {
     cudaStream_t s = g->stream;
     const int64_t n = g->n;
-    build_pass(g, d, nullptr);
+    const bool mg = g->comm && g->comm->nranks > 1;
+    const int64_t slots = mg ? (int64_t)g->comm->nranks * g->nb : n;
+    DevBuf<int32_t> deg;
+    deg.alloc((size_t)slots, s);
+    BFS_CUDA(cudaMemsetAsync(deg.p, 0, deg.bytes(), s));
+    k_local_degree<<<grid_for(g->nl(), 256), 256, 0, s>>>(g->off.p, g->nl(), deg.p + g->lo);
+    BFS_CHECK_LAUNCH();
+    if (mg) g->comm->allgather_inplace(deg.p, (size_t)g->nb * sizeof(int32_t), s);
     DevBuf<unsigned int> mx;
     mx.alloc(1, s);
     BFS_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(unsigned int), s));
-    k_degree_max<<<grid_for(n, 256), 256, 0, s>>>(g->off.p, n, mx.p);
+    k_degree_max<<<grid_for(n, 256), 256, 0, s>>>(deg.p, n, mx.p);
     BFS_CHECK_LAUNCH();
     unsigned int hmx = 0;
     BFS_CUDA(cudaMemcpyAsync(&hmx, mx.p, sizeof(hmx), cudaMemcpyDeviceToHost, s));
     BFS_CUDA(cudaStreamSynchronize(s));
     DevBuf<uint32_t> keys;
-    DevBuf<int32_t> order;
     keys.alloc((size_t)n, s);
     order.alloc((size_t)n, s);
-    k_degree_keys<<<grid_for(n, 256), 256, 0, s>>>(g->off.p, n, hmx, keys.p, order.p);
+    k_degree_keys<<<grid_for(n, 256), 256, 0, s>>>(deg.p, n, hmx, keys.p, order.p);
     BFS_CHECK_LAUNCH();
-    // pass-1 graph is no longer needed
-    g->adj.reset();
-    g->off.reset();
-    g->deg_raw.reset();
-    g->skip.reset();
-    g->head.reset();
+    deg.reset();
     const int bits = hmx ? 32 - __builtin_clz(hmx) : 0;
     radix_sort_pairs(keys.p, order.p, n, bits, s);
     keys.reset();
-    g->label.alloc((size_t)n, s);
-    g->ilabel.alloc((size_t)n, s);
-    k_labels<<<grid_for(n, 256), 256, 0, s>>>(order.p, n, g->label.p, g->ilabel.p);
+    rank.alloc((size_t)n, s);
+    k_rank_of<<<grid_for(n, 256), 256, 0, s>>>(order.p, n, rank.p);
     BFS_CHECK_LAUNCH();
-    order.reset();
-    build_pass(g, d, g->label.p);
-    g->reindexed = true;
+}
+
+static void finish_graph(bfs_graph_s* g) {
+    cudaStream_t s = g->stream;
+    const int64_t nl = g->nl();
+    const int64_t pw = padded_words(nl);
+    g->skip.alloc((size_t)pw, s);
+    k_skip_bits<<<grid_for(pw, 256), 256, 0, s>>>(g->off.p, nl, pw, g->skip.p);
+    BFS_CHECK_LAUNCH();
+    g->head.alloc((size_t)std::max<int64_t>(nl, 1), s);
+    k_head<<<grid_for(nl, 256), 256, 0, s>>>(g->off.p, g->adj.p, nl, g->head.p);
+    BFS_CHECK_LAUNCH();
+    BFS_CUDA(cudaStreamSynchronize(s));
+}
+
+void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
+    cudaStream_t s = g->stream;
+    build_pass(g, d, nullptr);
+    if (d->opts.reindex_by_degree) {
+        DevBuf<int32_t> rank, order;
+        degree_order(g, rank, order);
+        // pass-1 graph is no longer needed
+        g->adj.reset();
+        g->off.reset();
+        g->deg_raw.reset();
+        g->label = std::move(rank);
+        g->ilabel = std::move(order);
+        build_pass(g, d, g->label.p);
+        g->reindexed = true;
+    } else if (d->opts.sort_rows == 2) {
+        // rows in decreasing neighbour degree, ties by ID, labels
+        // unchanged: sort each row by the neighbour's degree rank, then map back
+        DevBuf<int32_t> rank, order;
+        degree_order(g, rank, order);
+        PhaseLog log;
+        k_map_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, rank.p);
+        BFS_CHECK_LAUNCH();
+        const bfs_build_opts keep = g->opts;
+        g->opts = bfs_build_opts{0, 0, 0, 1};
+        sort_and_compact(g);
+        g->opts = keep;
+        k_map_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, order.p);
+        BFS_CHECK_LAUNCH();
+        log.mark("degree row order", s);
+    }
+    finish_graph(g);
 }
 
 }  // namespace bfsb

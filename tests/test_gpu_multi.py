@@ -134,3 +134,20 @@ def test_fixtures_multi(p):
             for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
                 _check(gs, ref, root, pol, uv)
         _close(comms, gs)
+
+
+@pytest.mark.parametrize("p", [2, 4])
+def test_degree_row_order_multi(p):
+    scale, seed = 13, 3
+    uv, base = oracle.kron_graph(scale, 16, seed)
+    ref = oracle.sort_rows_by_degree(base)
+    opts = pkg.default_opts(sort_rows=2)
+    comms, gs = _build(p, lambda c, s: pkg.Graph.kronecker(scale, 16, seed, comm=c, stream=s, opts=opts))
+    for g in gs:
+        off, adj = g.export_csr()
+        lo, hi = g.local_begin, g.local_end
+        assert np.array_equal(adj.cpu().numpy(), ref.adj[ref.offsets[lo]:ref.offsets[hi]])
+    roots = oracle.sample_roots(ref, scale, seed, 4)
+    for r in roots:
+        _check(gs, ref, r, dict(mode=0), uv)
+    _close(comms, gs)

@@ -101,3 +101,20 @@ def test_radix_order_large_ties():
     new, _ = oracle.degree_reindex(ref, 1)
     assert np.array_equal(_labels(g), new)
     g.close()
+
+
+DEGROWS = dict(dedup=True, drop_self_loops=True, reindex_by_degree=False, sort_rows=2)
+
+
+@pytest.mark.parametrize("scale,abc,seed", [(14, oracle.KRON_ABC, 2), (12, oracle.ER_ABC, 5)])
+def test_degree_row_order(scale, abc, seed):
+    """sort_rows=2: rows by decreasing neighbour degree, labels unchanged"""
+    g = pkg.Graph.kronecker(scale, 16, seed, abc, opts=pkg.default_opts(**DEGROWS))
+    uv, base = oracle.kron_graph(scale, 16, seed, abc)
+    ref = oracle.sort_rows_by_degree(base)
+    off, adj = g.export_csr()
+    assert np.array_equal(off.cpu().numpy(), ref.offsets) and np.array_equal(adj.cpu().numpy(), ref.adj)
+    ident = np.arange(ref.n)
+    for i, r in enumerate(g.sample_roots(scale, seed, 6)):
+        _check(g, ref, ref, ident, r, [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1)][i % 3], uv)
+    g.close()

@@ -132,3 +132,26 @@ def test_relabel_preserves_structure(seed):
         d0, _ = oracle.bfs(g, root)
         d1, _ = oracle.bfs(r, int(new[root]))
         assert np.array_equal(d1[new], d0)
+
+
+def test_sort_rows_by_degree_spec():
+    n, uv = graphs.g1()
+    g = oracle.sort_rows_by_degree(oracle.build_csr(n, uv, sort_rows=True))
+    assert g.row(4).tolist() == [3, 5]        # degrees 2 > 1
+    assert g.row(1).tolist() == [0]           # S:193 singleton
+    assert g.row(0).tolist() == [3, 1, 2]     # degree 2 first, then the degree-1 tie by ID
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_sort_rows_by_degree_properties(seed):
+    n, uv = graphs.skewed_edges(300, 2500, seed)
+    base = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    g = oracle.sort_rows_by_degree(base)
+    deg = base.degree()
+    for v in range(n):
+        row = g.row(v).tolist()
+        assert sorted(row) == base.row(v).tolist()                          # multiset unchanged
+        keys = [(-deg[x], x) for x in row]
+        assert keys == sorted(keys)                                          # S:194 + ID tie-break
+    for root in (0, int(np.argmax(deg))):                                    # S:200 levels unchanged
+        assert np.array_equal(oracle.bfs(g, root)[0], oracle.bfs(base, root)[0])

@@ -19,11 +19,12 @@ ap.add_argument("--alphas", default="5,10,15,30,60")
 ap.add_argument("--betas", default="2,6,18,24")
 ap.add_argument("--roots", type=int, default=64)
 ap.add_argument("--reindex", type=int, default=0)
+ap.add_argument("--rows", type=int, default=1)
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)
 g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"],
-                        opts=pkg.default_opts(reindex_by_degree=bool(a.reindex)))
+                        opts=pkg.default_opts(reindex_by_degree=bool(a.reindex), sort_rows=a.rows))
 print("build_ms", g.build_ms, flush=True)
 roots = g.sample_roots(cfg["scale"], cfg["seed"], a.roots)
 parent = torch.empty(g.n, dtype=torch.int32, device="cuda")
