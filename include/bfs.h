@@ -219,6 +219,11 @@ bfs_status bfs_kronecker_edges(const bfs_kron_spec* spec, int64_t first, int64_t
 /* Local CSR (internal labels) into caller buffers (host or device):
  * offsets_out int64[local_n + 1] (starting at 0), adj_out int32[local arcs]. */
 bfs_status bfs_graph_export_csr(bfs_graph_t g, int64_t* offsets_out, int32_t* adj_out);
+/* One local row (internal labels) into a caller buffer (host or device): writes
+ * min(degree, cap) neighbours in stored order and *degree.  v is a local index
+ * in [0, local_end - local_begin).  Lets tests sample rows of graphs too large to
+ * export whole. */
+bfs_status bfs_graph_export_row(bfs_graph_t g, int64_t v, int32_t* out, int64_t cap, int64_t* degree);
 /* Internal label of every original vertex (identity unless reindexed), host or device int32[n]. */
 bfs_status bfs_graph_export_labels(bfs_graph_t g, int32_t* new_label_out);
 /* Root sampling (R8): candidates k = 0, 1, ... are Philox4x32-10

@@ -32,7 +32,7 @@ EXPORTS = ("bfs_graph_create", "bfs_graph_create_kronecker", "bfs_graph_create_e
            "bfs_graph_info", "bfs_graph_build_ms", "bfs_set_policy", "bfs_run", "bfs_stats", "bfs_graph_destroy",
            "bfs_comm_unique_id", "bfs_comm_create", "bfs_comm_create_local", "bfs_comm_destroy", "bfs_last_error",
            "bfs_kronecker_edges", "bfs_graph_export_csr", "bfs_graph_export_labels", "bfs_sample_roots",
-           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range")
+           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row")
 
 
 class BfsError(RuntimeError):
@@ -110,6 +110,7 @@ def lib() -> ctypes.CDLL:
             "bfs_sample_roots": [P, ctypes.c_uint32, ctypes.c_uint64, i64, P, P],
             "bfs_set_allocator": [P, P, P],
             "bfs_partition_range": [i64, i32, i32, P, P],
+            "bfs_graph_export_row": [P, i64, P, i64, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -221,6 +222,15 @@ def bfs_kronecker_edges(scale: int, edgefactor: int, seed: int, abc, first: int,
 
 def bfs_graph_export_csr(h, offsets_out, adj_out):
     _check(lib().bfs_graph_export_csr(h, _ptr(offsets_out), _ptr(adj_out)))
+
+
+def bfs_graph_export_row(h, v: int, cap: int = 1 << 20) -> np.ndarray:
+    """Local row v (stored order), at most cap neighbours, as a host int32 array."""
+    deg = ctypes.c_int64()
+    _check(lib().bfs_graph_export_row(h, v, None, 0, ctypes.byref(deg)))
+    out = np.empty(max(1, min(cap, deg.value)), np.int32)
+    _check(lib().bfs_graph_export_row(h, v, _ptr(out), min(cap, deg.value), ctypes.byref(deg)))
+    return out[: min(cap, deg.value)]
 
 
 def bfs_graph_export_labels(h, out):

@@ -383,6 +383,22 @@ bfs_status bfs_graph_export_csr(bfs_graph_t g, int64_t* offsets_out, int32_t* ad
     API_END
 }
 
+bfs_status bfs_graph_export_row(bfs_graph_t g, int64_t v, int32_t* out, int64_t cap, int64_t* degree) {
+    API_BEGIN
+    if (!g || !degree) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    if (v < 0 || v >= g->nl()) fail(BFS_ERR_OUT_OF_RANGE, "row outside the local range");
+    BFS_CUDA(cudaSetDevice(g->device));
+    int64_t be[2];
+    BFS_CUDA(cudaMemcpyAsync(be, g->off.p + v, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost, g->stream));
+    BFS_CUDA(cudaStreamSynchronize(g->stream));
+    *degree = be[1] - be[0];
+    const int64_t k = std::min<int64_t>(cap, be[1] - be[0]);
+    if (out && k > 0)
+        BFS_CUDA(cudaMemcpyAsync(out, g->adj.p + be[0], (size_t)k * sizeof(int32_t), cudaMemcpyDefault, g->stream));
+    BFS_CUDA(cudaStreamSynchronize(g->stream));
+    API_END
+}
+
 bfs_status bfs_graph_export_labels(bfs_graph_t g, int32_t* new_label_out) {
     API_BEGIN
     if (!g || !new_label_out) fail(BFS_ERR_INVALID_ARG, "NULL argument");
