@@ -276,7 +276,7 @@ def main():
         for r in roots:
             one(r)
             if int(r) not in edges:
-                edges[int(r)] = g.stats()[0]["component_edge_tuples"]
+                edges[int(r)] = pkg.bfs_component_tuples(g.h)
 
     times, launches = [], 0
     kern = {"bu": [0.0, 0, 0], "td": [0.0, 0, 0]}   # ms, bytes, launches
@@ -287,7 +287,7 @@ def main():
         for step in range(args.steps):
             for r in roots:
                 ms = one(r)
-                run, levels = g.stats()
+                run, levels = g.stats(tuples=False)
                 times.append(ms)
                 launches += run["kernel_launches"]
                 nvl_level_bytes += [lv["nvlink_bytes"] for lv in levels]

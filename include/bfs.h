@@ -176,10 +176,15 @@ bfs_status bfs_set_policy(bfs_graph_t g, const bfs_policy* policy);
  * root is not an error: one reached vertex, one step. */
 bfs_status bfs_run(bfs_graph_t g, int64_t root, int32_t* parent_out, int32_t* depth_out);
 
-/* Stats of the last bfs_run.  levels may be NULL; at most max_levels records are
- * copied (run_stats.levels says how many exist).  component_edge_tuples is
- * computed here, on the device, outside the timed region. */
+/* Stats of the last bfs_run (host copy only, no device work).  levels may be NULL;
+ * at most max_levels records are copied (run_stats.levels says how many exist).
+ * component_edge_tuples is -1 until bfs_component_tuples has been called for
+ * this run. */
 bfs_status bfs_stats(bfs_graph_t g, bfs_run_stats* out, bfs_level_stats* levels, int max_levels);
+/* TEPS numerator of the last bfs_run: input tuples with both endpoints reached
+ * (R5) = sum of raw degrees over reached vertices / 2, reduced on
+ * the device (collective on p ranks).  Meant to be called outside timed regions. */
+bfs_status bfs_component_tuples(bfs_graph_t g, int64_t* tuples);
 
 bfs_status bfs_graph_destroy(bfs_graph_t g);
 

@@ -32,7 +32,7 @@ EXPORTS = ("bfs_graph_create", "bfs_graph_create_kronecker", "bfs_graph_create_e
            "bfs_graph_info", "bfs_graph_build_ms", "bfs_set_policy", "bfs_run", "bfs_stats", "bfs_graph_destroy",
            "bfs_comm_unique_id", "bfs_comm_create", "bfs_comm_create_local", "bfs_comm_destroy", "bfs_last_error",
            "bfs_kronecker_edges", "bfs_graph_export_csr", "bfs_graph_export_labels", "bfs_sample_roots",
-           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row")
+           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row", "bfs_component_tuples")
 
 
 class BfsError(RuntimeError):
@@ -111,6 +111,7 @@ def lib() -> ctypes.CDLL:
             "bfs_set_allocator": [P, P, P],
             "bfs_partition_range": [i64, i32, i32, P, P],
             "bfs_graph_export_row": [P, i64, P, i64, P],
+            "bfs_component_tuples": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -199,6 +200,12 @@ def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_le
 
 def bfs_run(h, root: int, parent_out, depth_out):
     _check(lib().bfs_run(h, int(root), _ptr(parent_out), _ptr(depth_out)))
+
+
+def bfs_component_tuples(h) -> int:
+    t = ctypes.c_int64()
+    _check(lib().bfs_component_tuples(h, ctypes.byref(t)))
+    return t.value
 
 
 def bfs_stats(h, max_levels: int = 64):
@@ -339,7 +346,11 @@ class Graph:
         bfs_run(self.h, root, parent, depth)
         return parent, depth
 
-    def stats(self):
+    def stats(self, tuples: bool = True):
+        """(run, levels) of the last run; tuples=True also reduces the TEPS numerator
+        on the device (collective on p ranks; keep it out of timed loops)."""
+        if tuples:
+            bfs_component_tuples(self.h)
         return bfs_stats(self.h)
 
     def export_csr(self):

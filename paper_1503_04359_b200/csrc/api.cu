@@ -301,10 +301,19 @@ bfs_status bfs_stats(bfs_graph_t g, bfs_run_stats* out, bfs_level_stats* levels,
     if (!g || !out) fail(BFS_ERR_INVALID_ARG, "NULL argument");
     if (!g->has_run) fail(BFS_ERR_INVALID_ARG, "bfs_stats before any bfs_run");
     BFS_CUDA(cudaSetDevice(g->device));
-    if (g->run.component_edge_tuples < 0) g->run.component_edge_tuples = component_tuples_impl(g);
     *out = g->run;
     if (levels)
         for (int i = 0; i < max_levels && i < (int)g->levels.size(); ++i) levels[i] = g->levels[i];
+    API_END
+}
+
+bfs_status bfs_component_tuples(bfs_graph_t g, int64_t* tuples) {
+    API_BEGIN
+    if (!g || !tuples) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    if (!g->has_run) fail(BFS_ERR_INVALID_ARG, "bfs_component_tuples before any bfs_run");
+    BFS_CUDA(cudaSetDevice(g->device));
+    if (g->run.component_edge_tuples < 0) g->run.component_edge_tuples = component_tuples_impl(g);
+    *tuples = g->run.component_edge_tuples;
     API_END
 }
 

@@ -37,7 +37,7 @@ for alpha in [int(x) for x in a.alphas.split(",")]:
         rates = []
         for r in roots:
             pkg.bfs_run(g.h, int(r), parent, depth)
-            run, _ = g.stats()
+            run, _ = g.stats(tuples=True)
             rates.append(run["component_edge_tuples"] / (run["ms_total"] * 1e-3) / 1e9)
         res.append({"alpha": alpha, "beta": beta, "gteps": bench.hmean(rates)})
         print(json.dumps(res[-1]), flush=True)
