@@ -8,7 +8,7 @@
 //   visited u32[nl/32]    1 = visited or degree 0 (initialised from the skip mask)
 //   front / next u32[p*nb/32]  global frontier bitmaps; a rank writes its own slice
 //   q0 / q1 int32[nl]     frontier queues of owned vertices (global IDs)
-//   depth / parent int32[nl]   outputs, each entry written exactly once
+//   rec     int2[nl]      (depth, parent) recorded at discovery; k_emit writes the outputs
 //   (p > 1) seen u32[n/32] remote-claim dedup, out/in int2 claim lists
 //
 // Kernels:
@@ -24,7 +24,7 @@
 //   k_bu_batch    bottom-up step: warp per 32-word batch, per-lane rows with
 //                 kBuSlots in flight, warp-cooperative long rows (see below)
 //   k_q2b / k_b2q frontier queue <-> bitmap on direction switches
-//   k_finalize    parent = depth = -1 for unreached vertices (write-once outputs)
+//   k_emit        the output pass: depth/parent of every vertex written once, coalesced
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -71,7 +71,7 @@ __device__ __forceinline__ void queue_put(const Queue& q, unsigned long long pos
 
 // root_l < 0 on ranks that do not own the root
 __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int64_t root_l, int32_t root_g,
-                       int32_t* depth, int32_t* parent, Queue q, const int64_t* off, unsigned long long* cnt) {
+                       int2* out, int32_t root_o, Queue q, const int64_t* off, unsigned long long* cnt) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
         if (root_l >= 0 && w == (root_l >> 5)) x |= 1u << (root_l & 31);
@@ -80,8 +80,7 @@ __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int6
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         for (int i = 0; i < 16; ++i) cnt[i] = 0;
         if (root_l >= 0) {
-            depth[root_l] = 0;
-            parent[root_l] = root_g;
+            out[root_l] = make_int2(0, root_o);
             const int64_t b = off[root_l], e = off[root_l + 1];
             queue_put(q, 0, root_g, b, (int32_t)(e - b));
             cnt[C_NEXT] = 1;
@@ -124,7 +123,7 @@ template <bool kMulti>
 __global__ void __launch_bounds__(kTdThreads)
 k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
-            uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
+            uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
             const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo,
             int64_t hi, Remote rm) {
     __shared__ int64_t s_pre[kTdChunk + 2];
@@ -224,8 +223,7 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
                     s_q[slot] = v[j];
                     s_qb[slot] = b;
                     s_qd[slot] = (int32_t)(e - b);
-                    depth[vl] = next_level;
-                    parent[vl] = u[j];
+                    out[vl] = make_int2(next_level, pmap ? pmap[u[j]] : u[j]);
                     my_mf += (unsigned long long)(e - b);
                 }
             }
@@ -257,7 +255,7 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
 // Owner side of the top-down push: claims (v, parent) received from peers are
 // claimed exactly like local top-down targets (Alg. 2 "(local) ==> (remote)").
 __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t* __restrict__ off,
-                           uint32_t* __restrict__ visited, int32_t* __restrict__ depth, int32_t* __restrict__ parent,
+                           uint32_t* __restrict__ visited, int2* __restrict__ out,
                            const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level,
                            int64_t lo) {
     const int lane = threadIdx.x & 31;
@@ -283,8 +281,7 @@ __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t
                 const int64_t vl = c.x - lo;
                 const int64_t b = off[vl], e = off[vl + 1];
                 queue_put(qnext, base + __popc(m & lanemask_lt()), c.x, b, (int32_t)(e - b));
-                depth[vl] = next_level;
-                parent[vl] = c.y;
+                out[vl] = make_int2(next_level, c.y);
                 my_mf += (unsigned long long)(e - b);
             }
         }
@@ -321,8 +318,8 @@ constexpr int kLongCap = 64;
 __global__ void __launch_bounds__(kBuWarps * 32)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
-           const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int32_t* __restrict__ depth,
-           int32_t* __restrict__ parent, int64_t words, int64_t lo, int32_t next_level,
+           const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
+           const int32_t* __restrict__ pmap, int64_t words, int64_t lo, int32_t next_level,
            unsigned long long* __restrict__ cnt) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
@@ -410,8 +407,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                 if (sa[s]) {
                     my_insp += 1;
                     if (h[s]) {
-                        depth[vbase + sv[s]] = next_level;
-                        parent[vbase + sv[s]] = u[s];
+                        out[vbase + sv[s]] = make_int2(next_level, pmap ? pmap[u[s]] : u[s]);
                         atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
                         my_mf += (unsigned long long)sd[s];
                         sa[s] = false;
@@ -473,8 +469,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             }
             if (lane == 0) {
                 if (hit >= 0) {
-                    depth[vbase + lv] = next_level;
-                    parent[vbase + lv] = hu;
+                    out[vbase + lv] = make_int2(next_level, pmap ? pmap[hu] : hu);
                     nbw[lv >> 5] |= 1u << (lv & 31);
                     my_mf += (unsigned long long)s_ld[wid][x];
                     my_insp += (unsigned long long)(hit - jb + 1);
@@ -544,30 +539,25 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
     }
 }
 
-// unreached -> -1 (write-once outputs: discovered entries were written by the steps)
-__global__ void k_finalize(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip, int64_t nl,
-                           int64_t root_l, int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t w = v >> 5;
+// Output pass (the only writer of the caller's arrays): every entry of depth and
+// parent is written exactly once, in order, with full coalesced lines.  During
+// the traversal the steps record (depth, parent) of each discovered vertex as one
+// 8-byte `out` record in internal order; here reached vertices copy their record
+// and unreached ones get -1.
+//   one GPU / p ranks, labels unchanged: v = internal = original (owned slice)
+//   degree reindex: v runs over ORIGINAL labels, iv = label[v] gathers the record;
+//   isolated vertices sit at the tail of the internal order, so they skip the gather.
+__global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                       const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t count,
+                       int64_t root_l, int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < count; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t iv = label ? (int64_t)label[v] : v;
+        const int64_t w = iv >> 5;
         const uint32_t r = visited[w] & ~skip[w];
-        if (!((r >> (v & 31)) & 1u) && v != root_l) {
-            depth[v] = -1;
-            parent[v] = -1;
-        }
-    }
-}
-
-// original-label outputs from internal-label ones (degree reindex, one GPU)
-__global__ void k_remap_out(const int32_t* __restrict__ label, const int32_t* __restrict__ ilabel,
-                            const int32_t* __restrict__ dep_i, const int32_t* __restrict__ par_i, int64_t n,
-                            int32_t* __restrict__ dep_o, int32_t* __restrict__ par_o) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t iv = label[v];
-        if (dep_o) dep_o[v] = dep_i[iv];
-        if (par_o) {
-            const int32_t p = par_i[iv];
-            par_o[v] = p < 0 ? -1 : ilabel[p];
-        }
+        int2 o = make_int2(-1, -1);
+        if (((r >> (iv & 31)) & 1u) || iv == root_l) o = rec[iv];
+        if (depth) depth[v] = o.x;
+        if (parent) parent[v] = o.y;
     }
 }
 
@@ -632,6 +622,7 @@ void bfs_alloc_state(bfs_graph_s* g) {
     BFS_CUDA(cudaMemsetAsync(g->front.p, 0, g->front.bytes(), s));
     BFS_CUDA(cudaMemsetAsync(g->next.p, 0, g->next.bytes(), s));
     const size_t qcap = (size_t)std::max<int64_t>(nl, 1);
+    g->rec.alloc(qcap, s);
     g->q0.alloc(qcap, s);
     g->q1.alloc(qcap, s);
     g->qb0.alloc(qcap, s);
@@ -689,18 +680,21 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     const bool own_root = root_i >= g->lo && root_i < g->hi;
     const int64_t root_l = own_root ? root_i - g->lo : -1;
 
-    // where the kernels write (internal order, owned slice)
+    // the steps record (depth, parent) per discovered vertex in `rec` (internal
+    // order); k_emit writes the caller's arrays (device) or staging buffers (host)
     const bool dev_depth = depth_out && is_device_ptr(depth_out);
     const bool dev_parent = parent_out && is_device_ptr(parent_out);
-    int32_t* kd = (!g->reindexed && dev_depth) ? depth_out : nullptr;
-    int32_t* kp = (!g->reindexed && dev_parent) ? parent_out : nullptr;
-    if (!kd) {
+    int2* rec = g->rec.p;
+    const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
+    int32_t* od = dev_depth ? depth_out : nullptr;
+    int32_t* op = dev_parent ? parent_out : nullptr;
+    if (depth_out && !dev_depth) {
         if (!g->tmp_depth.p) g->tmp_depth.alloc((size_t)std::max<int64_t>(nl, 1), s);
-        kd = g->tmp_depth.p;
+        od = g->tmp_depth.p;
     }
-    if (!kp) {
+    if (parent_out && !dev_parent) {
         if (!g->tmp_parent.p) g->tmp_parent.alloc((size_t)std::max<int64_t>(nl, 1), s);
-        kp = g->tmp_parent.p;
+        op = g->tmp_parent.p;
     }
 
     g->levels.clear();
@@ -720,7 +714,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     const int64_t pw = padded_words(nl);
     Queue qcur{g->q0.p, g->qb0.p, g->qd0.p};
     Queue qnxt{g->q1.p, g->qb1.p, g->qd1.p};
-    k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, kd, kp, qcur,
+    k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, rec, (int32_t)root, qcur,
                                              g->off.p, cnt);
     BFS_CHECK_LAUNCH();
     ++launches;
@@ -790,11 +784,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 const int grid = grid_for(nchunks * kTdThreads, kTdThreads, 8);
                 if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
-                                                                  g->adj.p, g->visited.p, kd, kp, qnxt, cnt, d + 1,
+                                                                  g->adj.p, g->visited.p, rec, pmap, qnxt, cnt, d + 1,
                                                                   g->lo, g->hi, rm);
                 else
                     k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
-                                                                   g->off.p, g->adj.p, g->visited.p, kd, kp, qnxt, cnt,
+                                                                   g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, cnt,
                                                                    d + 1, g->lo, g->hi, rm);
                 BFS_CHECK_LAUNCH();
                 launches += 2;
@@ -823,7 +817,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 }
                 g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
                 if (R > 0) {
-                    k_td_merge<<<grid_for(R, 256), 256, 0, s>>>(g->in_list.p, R, g->off.p, g->visited.p, kd, kp, qnxt,
+                    k_td_merge<<<grid_for(R, 256), 256, 0, s>>>(g->in_list.p, R, g->off.p, g->visited.p, rec, qnxt,
                                                                 cnt, d + 1, g->lo);
                     BFS_CHECK_LAUNCH();
                     ++launches;
@@ -850,7 +844,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             const int64_t nbatches = (words + 31) / 32;
             k_bu_batch<<<grid_for(nbatches * 32, kBuWarps * 32, 8), kBuWarps * 32, 0, s>>>(
-                g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, kd, kp, words, g->lo, d + 1, cnt);
+                g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec, pmap, words, g->lo, d + 1, cnt);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;
@@ -880,28 +874,17 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     }
     const int ntimed = lt ? (int)std::min<size_t>(g->levels.size(), kMaxTimed) : 0;
     if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
-    k_finalize<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, nl, root_l, kd, kp);
-    BFS_CHECK_LAUNCH();
-    ++launches;
-    if (g->reindexed) {
-        int32_t* od = dev_depth ? depth_out : nullptr;
-        int32_t* op = dev_parent ? parent_out : nullptr;
-        DevBuf<int32_t> hd, hp;  // host outputs: remap into staging buffers, then copy
-        if (depth_out && !dev_depth) { hd.alloc((size_t)nl, s); od = hd.p; }
-        if (parent_out && !dev_parent) { hp.alloc((size_t)nl, s); op = hp.p; }
-        k_remap_out<<<grid_for(g->n, 256), 256, 0, s>>>(g->label.p, g->ilabel.p, kd, kp, g->n, od, op);
+    if (od || op) {
+        const int64_t count = g->reindexed ? g->n : nl;
+        k_emit<<<grid_for(count, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->reindexed ? g->label.p : nullptr,
+                                                    count, root_l, od, op);
         BFS_CHECK_LAUNCH();
         ++launches;
-        BFS_CUDA(cudaEventRecord(g->ev[1], s));
-        if (hd.p) BFS_CUDA(cudaMemcpyAsync(depth_out, hd.p, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
-        if (hp.p) BFS_CUDA(cudaMemcpyAsync(parent_out, hp.p, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
-        BFS_CUDA(cudaStreamSynchronize(s));
-    } else {
-        BFS_CUDA(cudaEventRecord(g->ev[1], s));
-        if (depth_out && !dev_depth) BFS_CUDA(cudaMemcpyAsync(depth_out, kd, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
-        if (parent_out && !dev_parent) BFS_CUDA(cudaMemcpyAsync(parent_out, kp, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
-        BFS_CUDA(cudaStreamSynchronize(s));
     }
+    BFS_CUDA(cudaEventRecord(g->ev[1], s));
+    if (depth_out && !dev_depth) BFS_CUDA(cudaMemcpyAsync(depth_out, od, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
+    if (parent_out && !dev_parent) BFS_CUDA(cudaMemcpyAsync(parent_out, op, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaStreamSynchronize(s));
     float ms = 0, ms_init = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
     BFS_CUDA(cudaEventElapsedTime(&ms_init, g->ev[0], g->ev[2]));

@@ -151,7 +151,8 @@ struct bfs_graph_s {
     bfsb::DevBuf<int64_t> prefix;    // [nl + 1] TD degree prefix
     bfsb::DevBuf<int64_t> cnt;       // [8] device counters
     int64_t* h_cnt = nullptr;        // pinned mirror
-    bfsb::DevBuf<int32_t> tmp_depth, tmp_parent;  // internal-label outputs / host staging
+    bfsb::DevBuf<int32_t> tmp_depth, tmp_parent;  // host-output staging
+    bfsb::DevBuf<int2> rec;          // [nl] (depth, parent) recorded at discovery, internal order
     bfsb::DevBuf<int64_t> scratch64; // TD chunk starts
     // 1D partition (p > 1)
     int64_t nb = 0;                  // block size: rank r owns [r*nb, min(n, (r+1)*nb))
