@@ -312,10 +312,11 @@ __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int
 //   5. the 32 next words are assembled in shared memory and stored coalesced.
 constexpr int kBuWarps = 8;
 constexpr int kBuSlots = 4;
+constexpr int kBuIlp = 4;
 constexpr int kBuLong = 8;
 constexpr int kLongCap = 64;
 
-__global__ void __launch_bounds__(kBuWarps * 32)
+__global__ void __launch_bounds__(kBuWarps * 32, 4)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
@@ -368,78 +369,106 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
         if (lane == 0) s_lcount[wid] = 0;
         my_scan += (unsigned long long)c;
         __syncwarp();
-        // 3. lane-serial scan with kBuSlots rows in flight per lane.  A row starts
-        //    "fresh": its first neighbour comes from the dense head record, so the
-        //    common first-probe hit never touches off[] or adj[]; only on a miss is
-        //    off[v] loaded and the rest of the row walked in adj[].
         const int64_t vbase = bt * 1024;
-        int t = lane;
-        int32_t sv[kBuSlots], sd[kBuSlots], su[kBuSlots];
-        int64_t sj[kBuSlots], se[kBuSlots];
-        bool sa[kBuSlots], sf[kBuSlots];
+        // 3a. first probes: every unvisited vertex tries the first neighbour of its
+        //     row from the dense head record (8 bytes, coalesced along the list);
+        //     kBuIlp records per lane are loaded before any is probed.  With rows in
+        //     canonical order this resolves most vertices.  Vertices that miss
+        //     and have more neighbours are compacted in place at the front of the list.
+        int M = 0;  // warp-uniform miss count
+        for (int t0 = 0; t0 < U; t0 += 32 * kBuIlp) {
+            int32_t sv[kBuIlp];
+            int2 hd[kBuIlp];
 #pragma unroll
-        for (int s = 0; s < kBuSlots; ++s) {
-            sa[s] = sf[s] = false;
-            sv[s] = sd[s] = su[s] = 0;
-            sj[s] = se[s] = 0;
-            if (t < U) {
-                sv[s] = list[t];
-                t += 32;
-                const int2 hd = __ldg(head + vbase + sv[s]);
-                su[s] = hd.x;
-                sd[s] = hd.y;
-                sa[s] = sf[s] = hd.y > 0;
+            for (int k = 0; k < kBuIlp; ++k) {
+                const int idx = t0 + k * 32 + lane;
+                sv[k] = idx < U ? (int32_t)list[idx] : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < kBuIlp; ++k) hd[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]) : make_int2(-1, 0);
+            bool hit[kBuIlp];
+#pragma unroll
+            for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front(front, hd[k].x);
+            __syncwarp();  // all lanes hold their entries of this block before misses overwrite it
+#pragma unroll
+            for (int k = 0; k < kBuIlp; ++k) {
+                if (hd[k].y > 0) my_insp += 1;
+                if (hit[k]) {
+                    out[vbase + sv[k]] = make_int2(next_level, pmap ? pmap[hd[k].x] : hd[k].x);
+                    atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
+                    my_mf += (unsigned long long)hd[k].y;
+                }
+                const bool miss = !hit[k] && hd[k].y > 1;
+                const unsigned mm = __ballot_sync(kFull, miss);
+                if (miss) list[M + __popc(mm & lanemask_lt())] = (uint16_t)sv[k];
+                M += __popc(mm);
             }
         }
-        for (;;) {
-            bool any = false;
-#pragma unroll
-            for (int s = 0; s < kBuSlots; ++s) any |= sa[s];
-            if (!__any_sync(kFull, any)) break;
-            int32_t u[kBuSlots];
-#pragma unroll
-            for (int s = 0; s < kBuSlots; ++s) u[s] = !sa[s] ? 0 : (sf[s] ? su[s] : __ldg(adj + sj[s]));
-            bool h[kBuSlots];
-#pragma unroll
-            for (int s = 0; s < kBuSlots; ++s) h[s] = sa[s] && in_front(front, u[s]);
+        __syncwarp();
+        // 3b. rows that missed: each lane keeps kBuSlots rows in flight from position 1
+        //     on and advances all of them each round (independent adj[j] loads, then
+        //     independent frontier probes), refilling a slot as soon as its row
+        //     resolves (the paper's "virtual warp" of one lane per vertex).
+        {
+            int t = lane;
+            int32_t sv[kBuSlots], sd[kBuSlots];
+            int64_t sj[kBuSlots], se[kBuSlots];
+            bool sa[kBuSlots];
 #pragma unroll
             for (int s = 0; s < kBuSlots; ++s) {
-                if (sa[s]) {
-                    my_insp += 1;
-                    if (h[s]) {
-                        out[vbase + sv[s]] = make_int2(next_level, pmap ? pmap[u[s]] : u[s]);
-                        atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
-                        my_mf += (unsigned long long)sd[s];
-                        sa[s] = false;
-                    } else if (sf[s]) {
-                        sf[s] = false;
-                        if (sd[s] == 1) {
-                            sa[s] = false;  // single neighbour, not in the frontier
-                        } else {
-                            const int64_t b = off[vbase + sv[s]];
-                            sj[s] = b + 1;
-                            se[s] = b + sd[s];
-                        }
-                    } else if (++sj[s] == se[s]) {
-                        sa[s] = false;  // exhausted: no frontier neighbour this level
-                    } else if (sd[s] - (se[s] - sj[s]) >= kBuLong) {
-                        const int idx = atomicAdd(s_lcount + wid, 1);
-                        if (idx < kLongCap) {  // hand the rest of the row to the warp
-                            s_lv[wid][idx] = sv[s];
-                            s_lj[wid][idx] = sj[s];
-                            s_le[wid][idx] = se[s];
-                            s_ld[wid][idx] = sd[s];
-                            sa[s] = false;
-                        }
-                    }
-                }
-                if (!sa[s] && t < U) {
+                sa[s] = false;
+                sv[s] = sd[s] = 0;
+                sj[s] = se[s] = 0;
+                if (t < M) {
                     sv[s] = list[t];
                     t += 32;
-                    const int2 hd = __ldg(head + vbase + sv[s]);
-                    su[s] = hd.x;
-                    sd[s] = hd.y;
-                    sa[s] = sf[s] = hd.y > 0;
+                    sd[s] = __ldg(head + vbase + sv[s]).y;
+                    sj[s] = off[vbase + sv[s]] + 1;
+                    se[s] = sj[s] - 1 + sd[s];
+                    sa[s] = true;
+                }
+            }
+            for (;;) {
+                bool any = false;
+#pragma unroll
+                for (int s = 0; s < kBuSlots; ++s) any |= sa[s];
+                if (!__any_sync(kFull, any)) break;
+                int32_t u[kBuSlots];
+#pragma unroll
+                for (int s = 0; s < kBuSlots; ++s) u[s] = sa[s] ? __ldg(adj + sj[s]) : 0;
+                bool h[kBuSlots];
+#pragma unroll
+                for (int s = 0; s < kBuSlots; ++s) h[s] = sa[s] && in_front(front, u[s]);
+#pragma unroll
+                for (int s = 0; s < kBuSlots; ++s) {
+                    if (sa[s]) {
+                        my_insp += 1;
+                        if (h[s]) {
+                            out[vbase + sv[s]] = make_int2(next_level, pmap ? pmap[u[s]] : u[s]);
+                            atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
+                            my_mf += (unsigned long long)sd[s];
+                            sa[s] = false;
+                        } else if (++sj[s] == se[s]) {
+                            sa[s] = false;  // exhausted: no frontier neighbour this level
+                        } else if (sd[s] - (se[s] - sj[s]) >= kBuLong) {
+                            const int idx = atomicAdd(s_lcount + wid, 1);
+                            if (idx < kLongCap) {  // hand the rest of the row to the warp
+                                s_lv[wid][idx] = sv[s];
+                                s_lj[wid][idx] = sj[s];
+                                s_le[wid][idx] = se[s];
+                                s_ld[wid][idx] = sd[s];
+                                sa[s] = false;
+                            }
+                        }
+                    }
+                    if (!sa[s] && t < M) {
+                        sv[s] = list[t];
+                        t += 32;
+                        sd[s] = __ldg(head + vbase + sv[s]).y;
+                        sj[s] = off[vbase + sv[s]] + 1;
+                        se[s] = sj[s] - 1 + sd[s];
+                        sa[s] = true;
+                    }
                 }
             }
         }
