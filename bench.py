@@ -214,8 +214,8 @@ def main():
     ap.add_argument("--alpha", type=int, default=30)
     ap.add_argument("--beta", type=int, default=24)
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--reindex", type=int, default=0, help="section 3.4 degree reindex (P:158)")
-    ap.add_argument("--rows", default="degree", choices=["id", "degree"],
+    ap.add_argument("--reindex", type=int, default=1, help="section 3.4 degree reindex (P:158)")
+    ap.add_argument("--rows", default="id", choices=["id", "degree"],
                     help="row order: ascending ID (sort_rows 1) or decreasing neighbour degree (2, P:158)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--levels-out", default=None, help="write per-level records (JSON) here")

@@ -576,17 +576,44 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
 //   one GPU / p ranks, labels unchanged: v = internal = original (owned slice)
 //   degree reindex: v runs over ORIGINAL labels, iv = label[v] gathers the record;
 //   isolated vertices sit at the tail of the internal order, so they skip the gather.
+// n_active: internal labels >= n_active are isolated (degree reindex puts them last)
+// and need neither the visited lookup nor the record gather.  Everything except the
+// visited bitmap is touched once, so it streams with evict-first hints and the
+// bitmap stays in L2 for the random lookups.
 __global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
-                       const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t count,
-                       int64_t root_l, int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < count; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t iv = label ? (int64_t)label[v] : v;
-        const int64_t w = iv >> 5;
+                       const int2* __restrict__ rec, int64_t nl, int64_t root_l, int32_t* __restrict__ depth,
+                       int32_t* __restrict__ parent) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = v >> 5;
         const uint32_t r = visited[w] & ~skip[w];
         int2 o = make_int2(-1, -1);
-        if (((r >> (iv & 31)) & 1u) || iv == root_l) o = rec[iv];
+        if (((r >> (v & 31)) & 1u) || v == root_l) o = rec[v];
         if (depth) depth[v] = o.x;
         if (parent) parent[v] = o.y;
+    }
+}
+
+// Degree-reindexed variant: v runs over ORIGINAL labels and gathers the record of
+// iv = label[v].  Internal labels >= n_active are isolated (the reindex puts them
+// last) and need neither the visited lookup nor the gather.  Everything except the
+// visited bitmap is touched once, so it streams with evict-first hints and the
+// bitmap stays in L2 for the random lookups.
+__global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                            const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
+                            int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
+                            int32_t* __restrict__ parent) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t iv = __ldcs(label + v);
+        int2 o = make_int2(-1, -1);
+        if (iv == root_l) {
+            o = rec[iv];
+        } else if (iv < n_active) {
+            const int64_t w = iv >> 5;
+            const uint32_t r = visited[w] & ~skip[w];
+            if ((r >> (iv & 31)) & 1u) o = __ldcs(rec + iv);
+        }
+        if (depth) __stcs(depth + v, o.x);
+        if (parent) __stcs(parent + v, o.y);
     }
 }
 
@@ -904,9 +931,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     const int ntimed = lt ? (int)std::min<size_t>(g->levels.size(), kMaxTimed) : 0;
     if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
     if (od || op) {
-        const int64_t count = g->reindexed ? g->n : nl;
-        k_emit<<<grid_for(count, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->reindexed ? g->label.p : nullptr,
-                                                    count, root_l, od, op);
+        if (g->reindexed)
+            k_emit_perm<<<grid_for(g->n, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->n,
+                                                            g->n_active, root_l, od, op);
+        else
+            k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, nl, root_l, od, op);
         BFS_CHECK_LAUNCH();
         ++launches;
     }

@@ -181,6 +181,14 @@ __global__ void k_degree_keys(const int32_t* deg, int64_t n, unsigned int mx, ui
     }
 }
 
+__global__ void k_count_active(const int64_t* off, int64_t nl, unsigned long long* cnt) {
+    unsigned long long c = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x)
+        c += off[v + 1] > off[v];
+    for (int d = 16; d > 0; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(cnt, c);
+}
+
 // order[k] = vertex at position k  ->  rank[vertex] = k
 __global__ void k_rank_of(const int32_t* order, int64_t n, int32_t* rank) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
@@ -751,6 +759,16 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         g->ilabel = std::move(order);
         build_pass(g, d, g->label.p);
         g->reindexed = true;
+        // isolated vertices are last in (degree desc, ID asc) order
+        DevBuf<unsigned long long> cntz;
+        cntz.alloc(1, s);
+        BFS_CUDA(cudaMemsetAsync(cntz.p, 0, sizeof(unsigned long long), s));
+        k_count_active<<<grid_for(g->nl(), 256), 256, 0, s>>>(g->off.p, g->nl(), cntz.p);
+        BFS_CHECK_LAUNCH();
+        unsigned long long act = 0;
+        BFS_CUDA(cudaMemcpyAsync(&act, cntz.p, sizeof(act), cudaMemcpyDeviceToHost, s));
+        BFS_CUDA(cudaStreamSynchronize(s));
+        g->n_active = (int64_t)act;
     } else if (d->opts.sort_rows == 2) {
         // rows in decreasing neighbour degree, ties by ID, labels
         // unchanged: sort each row by the neighbour's degree rank, then map back

@@ -138,6 +138,7 @@ struct bfs_graph_s {
     bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path
     // reindex (identity when absent)
     bool reindexed = false;
+    int64_t n_active = 0;            // reindexed: labels >= n_active are isolated
     bfsb::DevBuf<int32_t> label;    // [n] original -> internal
     bfsb::DevBuf<int32_t> ilabel;   // [n] internal -> original
 
