@@ -1,14 +1,14 @@
 """Full-size parity, in the launch configuration bench.py times (BASELINE.json
-configs K26 and K29: Kronecker, edgefactor 16, rows by decreasing neighbour
-degree, alpha 30 / beta 24).
+configs K26 and K29: Kronecker, edgefactor 16, section 3.4 degree reindex with
+rows by decreasing neighbour degree, alpha 30 / beta 24).
 
 The serial oracle cannot build these graphs in test time, so the checks use what
 it CAN compute one by one plus properties that hold at any size:
   * generator: sampled edge ranges, oracle Philox generator vs the GPU, bit-exact;
-  * CSR: every sampled oracle edge {u, v} is present in the GPU row of its
-    lower-degree endpoint (self-loops dropped), sampled rows are duplicate-free
-    and in the degree order, and sum of CSR degrees = 2 * (distinct non-loop edges)
-    is consistent with the arc count;
+  * CSR (internal labels; the label map is checked to be a permutation that
+    orders vertices by non-increasing degree): every sampled oracle edge {u, v}
+    is present in the GPU row of its lower-degree endpoint (self-loops dropped),
+    sampled rows are duplicate-free and in the degree order;
   * BFS: V1 and V5 on every vertex, V3 (depth[parent] = depth - 1) on every
     reached vertex, V2 (tree edge exists) on sampled vertices against the checked
     rows, V4 (no edge spans more than one level) on sampled oracle edges, and the
@@ -56,11 +56,19 @@ def test_fullscale_properties(name):
         samples.append(want)
     edges = np.concatenate(samples)   # 512K oracle edges for the V4 check
 
-    g = pkg.Graph.kronecker(scale, ef, seed, abc, opts=pkg.default_opts(sort_rows=2))
+    g = pkg.Graph.kronecker(scale, ef, seed, abc, opts=pkg.default_opts(reindex_by_degree=True))
     g.set_policy(mode=0, alpha=30, beta=24)
+    lab = torch.empty(n, dtype=torch.int32, device="cuda")
+    pkg.bfs_graph_export_labels(g.h, lab)
+    label = lab.cpu().numpy()
+    del lab
+    assert np.array_equal(np.sort(label), np.arange(n, dtype=np.int32))       # a permutation
 
-    def row(v):
-        return pkg.bfs_graph_export_row(g.h, int(v), cap=1 << 24)
+    def row(v):  # row of ORIGINAL vertex v, as original labels
+        return ilabel[pkg.bfs_graph_export_row(g.h, int(label[v]), cap=1 << 24)]
+
+    ilabel = np.empty(n, np.int32)
+    ilabel[label] = np.arange(n, dtype=np.int32)
 
     # CSR: sampled edges present in the row of the lower-degree endpoint
     deg_cache = {}
@@ -81,6 +89,11 @@ def test_fullscale_properties(name):
         assert len(np.unique(r)) == len(r) and a not in r                    # dedup, no self-loops
         d = np.array([deg(int(x)) for x in r[:64]])
         assert np.all(d[:-1] >= d[1:])                                         # decreasing degree
+        assert np.all(np.diff(label[r]) > 0)                                   # ties by (internal) ID
+    # internal order = degree order on sampled vertices
+    smp = np.sort(rng.choice(n, 200, replace=False))
+    ds = np.array([deg(int(ilabel[x])) for x in smp])
+    assert np.all(ds[:-1] >= ds[1:])
 
     roots = g.sample_roots(scale, seed, 2)
     depth_h = torch.empty(n, dtype=torch.int32).pin_memory()
