@@ -321,7 +321,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
            const int32_t* __restrict__ pmap, int64_t words, int64_t lo, int32_t next_level,
-           unsigned long long* __restrict__ cnt) {
+           unsigned long long* __restrict__ cnt, int grab) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
     __shared__ int64_t s_lj[kBuWarps][kLongCap];
@@ -335,11 +335,18 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
     const int64_t wbase = lo >> 5;
     const int64_t nbatches = (words + 31) / 32;
     unsigned long long my_nf = 0, my_mf = 0, my_insp = 0, my_scan = 0;
-    for (;;) {
-        long long bt = 0;
-        if (lane == 0) bt = (long long)atomicAdd(cnt + C_WORK, 1ull);
-        bt = __shfl_sync(kFull, bt, 0);
-        if (bt >= nbatches) break;
+    // batches are claimed `grab` at a time from the global counter (one atomic per
+    // grab: a sparse level is otherwise bound by that single address)
+    long long bt = 0, bt_end = 0;
+    for (;; ++bt) {
+        if (bt >= bt_end) {
+            long long g0 = 0;
+            if (lane == 0) g0 = (long long)atomicAdd(cnt + C_WORK, (unsigned long long)grab);
+            g0 = __shfl_sync(kFull, g0, 0);
+            if (g0 >= nbatches) break;
+            bt = g0;
+            bt_end = min(g0 + (long long)grab, (long long)nbatches);
+        }
         const int64_t w = bt * 32 + lane;
         const uint32_t vis = w < words ? visited[w] : kFull;
         const uint32_t un = ~vis;
@@ -602,18 +609,44 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
                             const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
                             int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
                             int32_t* __restrict__ parent) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t iv = __ldcs(label + v);
-        int2 o = make_int2(-1, -1);
-        if (iv == root_l) {
-            o = rec[iv];
-        } else if (iv < n_active) {
-            const int64_t w = iv >> 5;
-            const uint32_t r = visited[w] & ~skip[w];
-            if ((r >> (iv & 31)) & 1u) o = __ldcs(rec + iv);
+    // 4 consecutive original vertices per thread: one 16-byte label load, four
+    // independent lookup/gather chains in flight, 16-byte output stores
+    const bool vec = ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(parent)) & 15) == 0 &&
+                     depth && parent;
+    const int64_t quads = (n + 3) / 4;
+    for (int64_t qd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qd < quads; qd += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v0 = qd * 4;
+        int32_t iv[4];
+        if (v0 + 4 <= n) {
+            const int4 l4 = __ldcs(reinterpret_cast<const int4*>(label + v0));
+            iv[0] = l4.x; iv[1] = l4.y; iv[2] = l4.z; iv[3] = l4.w;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) iv[k] = v0 + k < n ? label[v0 + k] : -1;
         }
-        if (depth) __stcs(depth + v, o.x);
-        if (parent) __stcs(parent + v, o.y);
+        uint32_t r[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            r[k] = 0;
+            if (iv[k] >= 0 && iv[k] < n_active) r[k] = visited[iv[k] >> 5] & ~skip[iv[k] >> 5];
+        }
+        int2 o[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            o[k] = make_int2(-1, -1);
+            if (iv[k] >= 0 && (((r[k] >> (iv[k] & 31)) & 1u) || iv[k] == root_l)) o[k] = __ldcs(rec + iv[k]);
+        }
+        if (vec && v0 + 4 <= n) {
+            __stcs(reinterpret_cast<int4*>(depth + v0), make_int4(o[0].x, o[1].x, o[2].x, o[3].x));
+            __stcs(reinterpret_cast<int4*>(parent + v0), make_int4(o[0].y, o[1].y, o[2].y, o[3].y));
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (v0 + k >= n) break;
+                if (depth) depth[v0 + k] = o[k].x;
+                if (parent) parent[v0 + k] = o[k].y;
+            }
+        }
     }
 }
 
@@ -899,8 +932,10 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             const int64_t nbatches = (words + 31) / 32;
-            k_bu_batch<<<grid_for(nbatches * 32, kBuWarps * 32, 8), kBuWarps * 32, 0, s>>>(
-                g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec, pmap, words, g->lo, d + 1, cnt);
+            const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, 4);
+            const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
+            k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
+                                                         pmap, words, g->lo, d + 1, cnt, grab);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;
