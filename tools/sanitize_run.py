@@ -1,0 +1,45 @@
+"""Small end-to-end workload for compute-sanitizer (memcheck / racecheck /
+synccheck): every kernel path (build, sort classes incl. merge, reindex, degree
+rows, TD/BU/conversions, output passes, multi-partition local transport)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1503_04359_b200 as pkg  # noqa: E402
+
+torch.cuda.set_device(0)
+rng = np.random.default_rng(0)
+for opts in (pkg.default_opts(), pkg.default_opts(reindex_by_degree=True), pkg.default_opts(sort_rows=2),
+             pkg.default_opts(False, False, False, 1)):
+    g = pkg.Graph.kronecker(11, 16, 3, opts=opts)
+    for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
+        g.set_policy(**pol)
+        for r in g.sample_roots(11, 3, 3):
+            g.run(int(r))
+            g.stats()
+    g.close()
+# a hub row longer than the shared-memory sort (merge path)
+n = 1 << 16
+uv = np.concatenate([np.stack([np.zeros(40000, np.int64), rng.integers(0, n, 40000)], 1),
+                     rng.integers(0, n, size=(20000, 2))]).astype(np.int32)
+g = pkg.Graph.from_edges(uv, n)
+g.run(0)
+h = np.empty(n, np.int32)
+pkg.bfs_run(g.h, 0, h, None)
+g.close()
+# multi-partition (local transport)
+comms = pkg.bfs_comm_create_local(3, 0)
+gs = pkg.run_ranks(lambda r: pkg.Graph.kronecker(10, 16, 2, comm=comms[r], stream=torch.cuda.Stream()), 3)
+def go(r):
+    torch.cuda.set_device(0)
+    gs[r].run(5)
+    return gs[r].stats()
+pkg.run_ranks(go, 3)
+for x in gs:
+    x.close()
+print("sanitize workload done")
