@@ -320,7 +320,8 @@ __global__ void __launch_bounds__(kBuWarps * 32, 4)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
-           const int32_t* __restrict__ pmap, int64_t words, int64_t lo, int32_t next_level,
+           const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
+           int32_t next_level,
            unsigned long long* __restrict__ cnt, int grab) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
@@ -393,6 +394,12 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             }
 #pragma unroll
             for (int k = 0; k < kBuIlp; ++k) hd[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]) : make_int2(-1, 0);
+            // reindexed graphs: the first neighbour's ORIGINAL label comes from a dense
+            // per-vertex array read beside the head record (coalesced), not from a
+            // random ilabel[] lookup after the probe
+            int32_t po[kBuIlp];
+#pragma unroll
+            for (int k = 0; k < kBuIlp; ++k) po[k] = (hpar && sv[k] >= 0) ? __ldg(hpar + vbase + sv[k]) : hd[k].x;
             bool hit[kBuIlp];
 #pragma unroll
             for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front(front, hd[k].x);
@@ -401,7 +408,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             for (int k = 0; k < kBuIlp; ++k) {
                 if (hd[k].y > 0) my_insp += 1;
                 if (hit[k]) {
-                    out[vbase + sv[k]] = make_int2(next_level, pmap ? pmap[hd[k].x] : hd[k].x);
+                    out[vbase + sv[k]] = make_int2(next_level, po[k]);
                     atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
                     my_mf += (unsigned long long)hd[k].y;
                 }
@@ -972,7 +979,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, 4);
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
-                                                         pmap, words, g->lo, d + 1, cnt, grab);
+                                                         pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
+                                                         d + 1, cnt, grab);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;

@@ -160,6 +160,15 @@ __global__ void k_head(const int64_t* off, const int32_t* adj, int64_t nl, int2*
     }
 }
 
+// hpar[v] = original label of v's first neighbour (reindexed graphs): the parent a
+// first-probe bottom-up hit writes, read coalesced beside head[v]
+__global__ void k_head_parent(const int2* head, const int32_t* ilabel, int64_t nl, int32_t* hpar) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t f = head[v].x;
+        hpar[v] = f >= 0 ? ilabel[f] : -1;
+    }
+}
+
 // degree-order helpers: key = maxdeg - deg (ascending key = descending degree)
 __global__ void k_local_degree(const int64_t* off, int64_t nl, int32_t* deg) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x)
@@ -742,6 +751,11 @@ static void finish_graph(bfs_graph_s* g) {
     g->head.alloc((size_t)std::max<int64_t>(nl, 1), s);
     k_head<<<grid_for(nl, 256), 256, 0, s>>>(g->off.p, g->adj.p, nl, g->head.p);
     BFS_CHECK_LAUNCH();
+    if (g->reindexed) {
+        g->hpar.alloc((size_t)std::max<int64_t>(nl, 1), s);
+        k_head_parent<<<grid_for(nl, 256), 256, 0, s>>>(g->head.p, g->ilabel.p, nl, g->hpar.p);
+        BFS_CHECK_LAUNCH();
+    }
     BFS_CUDA(cudaStreamSynchronize(s));
 }
 

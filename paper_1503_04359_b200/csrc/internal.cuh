@@ -136,6 +136,7 @@ struct bfs_graph_s {
     bfsb::DevBuf<int32_t> deg_raw;  // [nl] raw arcs per vertex (TEPS numerator)
     bfsb::DevBuf<uint32_t> skip;    // [padded words of nl] bit set = CSR degree 0
     bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path
+    bfsb::DevBuf<int32_t> hpar;     // [nl] reindexed only: ORIGINAL label of the first neighbour
     // reindex (identity when absent)
     bool reindexed = false;
     int64_t n_active = 0;            // reindexed: labels >= n_active are isolated
