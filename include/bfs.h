@@ -84,6 +84,11 @@ typedef struct {
  *           n_f(d)*beta < n and n_f(d) < n_f(d-1).  Integer arithmetic only.
  *   mode 1  TD only (classic BFS, "top-down (classic)")
  *   mode 2  TD for steps d < bu_from_level, BU for every step d >= bu_from_level
+ *   mode 3  the paper's own rule (section 3.3; R23):
+ *           in TD go BU iff m_fc(d)*10000 >= alpha*arcs, m_fc = degree sum of the
+ *           frontier vertices partition 0 (the coordinator) owns, alpha = the
+ *           "static percent" in units of 1/10000 (500 = 0.05); after beta BU
+ *           steps ("a fixed number of steps") return to TD for the rest of the search.
  * level_times != 0 records a CUDA-event time per step into bfs_level_stats.ms.
  * Defaults: mode 0, alpha 15, beta 18, bu_from_level 0, level_times 0. */
 typedef struct {

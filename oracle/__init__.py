@@ -74,7 +74,7 @@ def _L():
             lib.orc_bfs.restype = i64
             lib.orc_validate.argtypes = [i64, P, P, i64, P, P, P, P, P]
             lib.orc_validate.restype = i64
-            lib.orc_do_emulate.argtypes = [i64, P, P, P, i64, i64, i32, i64, i64, P, P, P, P, P, P, P]
+            lib.orc_do_emulate.argtypes = [i64, P, P, P, i64, i64, i32, i64, i64, P, P, P, P, P, P, P, i64]
             lib.orc_do_emulate.restype = i64
             lib.orc_component_tuples.argtypes = [i64, P, P]
             lib.orc_component_tuples.restype = i64
@@ -220,8 +220,9 @@ def validate(g: CSR, root: int, depth, parent, ref_depth=None) -> dict:
 
 
 def do_emulate(g: CSR, depth, alpha: int = 15, beta: int = 18, policy: int = 0, bu_from: int = 0,
-               want_bu_parent: bool = False) -> dict:
-    """Per-step direction, n_f, m_f, m_u, discovered and inspections (see oracle.c)."""
+               want_bu_parent: bool = False, coord_hi: int | None = None) -> dict:
+    """Per-step direction, n_f, m_f, m_u, discovered and inspections (see oracle.c).
+    coord_hi: policy 3's coordinator owns labels [0, coord_hi) (default: all)."""
     d = _c(depth, np.int32)
     S = int(d.max()) + 2 if d.size else 2
     dirs = np.zeros(S, np.int32)
@@ -229,7 +230,8 @@ def do_emulate(g: CSR, depth, alpha: int = 15, beta: int = 18, policy: int = 0, 
     bp = np.zeros(g.n, np.int32) if want_bu_parent else None
     adj = g.adj if g.arcs else np.zeros(1, np.int32)
     steps = _L().orc_do_emulate(g.n, _p(g.offsets), _p(adj), _p(d), alpha, beta, policy, bu_from, S,
-                                _p(dirs), *[_p(a) for a in arrs], _p(bp) if bp is not None else None)
+                                _p(dirs), *[_p(a) for a in arrs], _p(bp) if bp is not None else None,
+                                g.n if coord_hi is None else int(coord_hi))
     assert steps >= 0
     out = {"dir": dirs[:steps], "n_f": arrs[0][:steps], "m_f": arrs[1][:steps], "m_u": arrs[2][:steps],
            "discovered": arrs[3][:steps], "insp": arrs[4][:steps]}

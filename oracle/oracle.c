@@ -366,7 +366,14 @@ int64_t orc_validate(int64_t n, const int64_t* offsets, const int32_t* adj, int6
  * and the direction the integer rule picks (start TD):
  *   mode TD: go BU for step d iff m_f(d) * alpha > m_u(d)
  *   mode BU: go TD for step d iff n_f(d) * beta < n  and  n_f(d) < n_f(d-1)
- * Policy: 0 = auto (rule above), 1 = TD only, 2 = BU for every step d >= bu_from.
+ * Policy: 0 = auto (rule above), 1 = TD only, 2 = BU for every step d >= bu_from,
+ *   3 = the paper's own rule (section 3.3; R23):
+ *       TD -> BU for step d iff m_fc(d) * 10000 >= alpha * arcs, where m_fc(d) is the
+ *       degree sum of the frontier vertices the coordinator partition owns (labels
+ *       [0, coord_hi); "the coordinator for switching can be the partition
+ *       responsible for the high degree vertices") and alpha is the "static
+ *       percent" in units of 1/10000; BU -> TD after beta BU steps ("a fixed number
+ *       of steps"), never BU again.
  * Inspections of step d: TD -> m_f(d) (every arc of every frontier vertex).
  *   BU -> sum over v with depth > d or unreached, deg(v) > 0, of
  *         (index of v's first neighbour with depth d) + 1, or deg(v) if none
@@ -380,7 +387,7 @@ int64_t orc_validate(int64_t n, const int64_t* offsets, const int32_t* adj, int6
 int64_t orc_do_emulate(int64_t n, const int64_t* offsets, const int32_t* adj, const int32_t* depth,
                        int64_t alpha, int64_t beta, int policy, int64_t bu_from, int64_t max_steps,
                        int32_t* dir, int64_t* n_f, int64_t* m_f, int64_t* m_u, int64_t* discovered,
-                       int64_t* insp, int32_t* bu_parent) {
+                       int64_t* insp, int32_t* bu_parent, int64_t coord_hi) {
     int32_t maxd = -1;
     int64_t arcs = offsets[n];
     for (int64_t v = 0; v < n; ++v) if (depth[v] > maxd) maxd = depth[v];
@@ -389,9 +396,15 @@ int64_t orc_do_emulate(int64_t n, const int64_t* offsets, const int32_t* adj, co
     if (bu_parent) for (int64_t v = 0; v < n; ++v) bu_parent[v] = -1;
     int64_t* cnt = (int64_t*)calloc((size_t)steps + 1, sizeof(int64_t));
     int64_t* dsum = (int64_t*)calloc((size_t)steps + 1, sizeof(int64_t));
+    int64_t* csum = (int64_t*)calloc((size_t)steps + 1, sizeof(int64_t)); /* coordinator's share */
     for (int64_t v = 0; v < n; ++v)
-        if (depth[v] >= 0) { cnt[depth[v]] += 1; dsum[depth[v]] += offsets[v + 1] - offsets[v]; }
+        if (depth[v] >= 0) {
+            cnt[depth[v]] += 1;
+            dsum[depth[v]] += offsets[v + 1] - offsets[v];
+            if (v < coord_hi) csum[depth[v]] += offsets[v + 1] - offsets[v];
+        }
     int mode = 0; /* 0 TD, 1 BU */
+    int64_t bu_done = 0, returned = 0; /* policy 3: BU steps taken; back in TD for good */
     int64_t seen_deg = 0;
     for (int64_t d = 0; d < steps; ++d) {
         seen_deg += dsum[d];
@@ -401,7 +414,11 @@ int64_t orc_do_emulate(int64_t n, const int64_t* offsets, const int32_t* adj, co
         discovered[d] = cnt[d + 1];
         if (policy == 1) mode = 0;
         else if (policy == 2) mode = (d >= bu_from) ? 1 : 0;
-        else {
+        else if (policy == 3) {
+            if (mode == 0) { if (!returned && csum[d] * 10000 >= alpha * arcs) mode = 1; }
+            else if (bu_done >= beta) { mode = 0; returned = 1; }
+            if (mode == 1) bu_done += 1;
+        } else {
             if (mode == 0) { if (m_f[d] * alpha > m_u[d]) mode = 1; }
             else { if (n_f[d] * beta < n && n_f[d] < n_f[d - 1]) mode = 0; }
         }
@@ -429,6 +446,7 @@ int64_t orc_do_emulate(int64_t n, const int64_t* offsets, const int32_t* adj, co
     }
     free(cnt);
     free(dsum);
+    free(csum);
     return steps;
 }
 

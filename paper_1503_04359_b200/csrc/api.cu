@@ -279,7 +279,7 @@ bfs_status bfs_graph_build_ms(bfs_graph_t g, double* ms) {
 bfs_status bfs_set_policy(bfs_graph_t g, const bfs_policy* p) {
     API_BEGIN
     if (!g || !p) fail(BFS_ERR_INVALID_ARG, "NULL argument");
-    if (p->mode < 0 || p->mode > 2) fail(BFS_ERR_INVALID_ARG, "policy.mode must be 0, 1 or 2");
+    if (p->mode < 0 || p->mode > 3) fail(BFS_ERR_INVALID_ARG, "policy.mode must be 0, 1, 2 or 3");
     if (p->alpha < 1 || p->alpha > (1 << 24) || p->beta < 1 || p->beta > (1 << 24))
         fail(BFS_ERR_INVALID_ARG, "alpha and beta must be in [1, 2^24]");
     if (p->bu_from_level < 0) fail(BFS_ERR_INVALID_ARG, "bu_from_level must be >= 0");

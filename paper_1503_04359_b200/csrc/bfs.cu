@@ -40,7 +40,8 @@ constexpr int kTdItems = 4;
 constexpr int kTdChunk = kTdThreads * kTdItems;  // arcs per CTA iteration
 
 // counter slots: [0, 8) written by this rank's kernels, [8, 16) global (allreduced)
-enum { C_NEXT = 0, C_MF = 1, C_INSP = 2, C_B2Q = 3, C_SCAN = 4, C_WORK = 5, C_TUPLES = 6, C_GLOBAL = 8 };
+enum { C_NEXT = 0, C_MF = 1, C_INSP = 2, C_B2Q = 3, C_SCAN = 4, C_WORK = 5, C_TUPLES = 6, C_COORD = 7,
+       C_GLOBAL = 8 };
 
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned r;
@@ -54,24 +55,23 @@ __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x)
     return x;
 }
 
-// A top-down frontier queue: vertex (global ID) plus its row begin and degree,
-// recorded when the vertex is discovered (its offsets are read then anyway) so
-// that expanding it never re-reads `off` at random.
+// A top-down frontier queue: vertex (global ID) plus its degree, read from the
+// vertex's 8-byte head record when it is discovered (one sector; the degree feeds
+// m_f of the next frontier).  The row begin is read only if the queue is expanded
+// top-down (a TD level followed by a BU level never needs it).
 struct Queue {
     int32_t* v;
-    int64_t* beg;
     int32_t* deg;
 };
 
-__device__ __forceinline__ void queue_put(const Queue& q, unsigned long long pos, int32_t v, int64_t beg, int32_t deg) {
-    q.v[pos] = v;
-    q.beg[pos] = beg;
-    q.deg[pos] = deg;
+__device__ __forceinline__ void queue_put(const Queue& q, unsigned long long pos, int32_t v, int32_t deg) {
+    __stcs(q.v + pos, v);
+    __stcs(q.deg + pos, deg);
 }
 
 // root_l < 0 on ranks that do not own the root
 __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int64_t root_l, int32_t root_g,
-                       int2* out, int32_t root_o, Queue q, const int64_t* off, unsigned long long* cnt) {
+                       int2* out, int32_t root_o, Queue q, const int2* head, unsigned long long* cnt) {
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
         if (root_l >= 0 && w == (root_l >> 5)) x |= 1u << (root_l & 31);
@@ -81,10 +81,10 @@ __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int6
         for (int i = 0; i < 16; ++i) cnt[i] = 0;
         if (root_l >= 0) {
             out[root_l] = make_int2(0, root_o);
-            const int64_t b = off[root_l], e = off[root_l + 1];
-            queue_put(q, 0, root_g, b, (int32_t)(e - b));
+            const int32_t dg = head[root_l].y;
+            queue_put(q, 0, root_g, dg);
             cnt[C_NEXT] = 1;
-            cnt[C_MF] = (unsigned long long)(e - b);
+            cnt[C_MF] = (unsigned long long)dg;
         }
     }
 }
@@ -124,13 +124,12 @@ __global__ void __launch_bounds__(kTdThreads)
 k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
-            const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo,
-            int64_t hi, Remote rm) {
+            const Queue qnext, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
+            int32_t next_level, int64_t lo, int64_t hi, Remote rm) {
     __shared__ int64_t s_pre[kTdChunk + 2];
     __shared__ int64_t s_beg[kTdChunk + 1];
     __shared__ int32_t s_u[kTdChunk + 1];
     __shared__ int32_t s_q[kTdChunk];
-    __shared__ int64_t s_qb[kTdChunk];
     __shared__ int32_t s_qd[kTdChunk];
     __shared__ int s_qn;
     __shared__ unsigned long long s_base;
@@ -149,8 +148,9 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
             for (int k = threadIdx.x; k <= cntv; k += kTdThreads) {
                 s_pre[k] = prefix[i0 + k];
                 if (k < cntv) {
-                    s_u[k] = q.v[i0 + k];
-                    s_beg[k] = q.beg[i0 + k];
+                    const int32_t uu = q.v[i0 + k];
+                    s_u[k] = uu;
+                    s_beg[k] = off[uu - lo];
                 }
             }
         }
@@ -182,10 +182,10 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
                         else b = mid - 1;
                     }
                     u[j] = q.v[a];
-                    beg = q.beg[a];
+                    beg = off[u[j] - lo];
                     pre = prefix[a];
                 }
-                v[j] = __ldg(adj + beg + (e - pre));
+                v[j] = __ldcs(adj + beg + (e - pre));   // streamed once: evict-first
             }
         }
         // B: probe, then claim.  Owned targets in `visited`, remote ones in `seen`.
@@ -219,12 +219,11 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
                 if (lw) {
                     const int64_t vl = v[j] - lo;
                     const int slot = base + __popc(m & lanemask_lt());
-                    const int64_t b = off[vl], e = off[vl + 1];
+                    const int32_t dg = __ldg(head + vl).y;
                     s_q[slot] = v[j];
-                    s_qb[slot] = b;
-                    s_qd[slot] = (int32_t)(e - b);
+                    s_qd[slot] = dg;
                     out[vl] = make_int2(next_level, pmap ? pmap[u[j]] : u[j]);
-                    my_mf += (unsigned long long)(e - b);
+                    my_mf += (unsigned long long)dg;
                 }
             }
             if (kMulti) {
@@ -244,7 +243,7 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
         const int qn = s_qn;
         if (threadIdx.x == 0 && qn) s_base = atomicAdd(cnt + C_NEXT, (unsigned long long)qn);
         __syncthreads();
-        for (int k = threadIdx.x; k < qn; k += kTdThreads) queue_put(qnext, s_base + k, s_q[k], s_qb[k], s_qd[k]);
+        for (int k = threadIdx.x; k < qn; k += kTdThreads) queue_put(qnext, s_base + k, s_q[k], s_qd[k]);
         __syncthreads();
         if (threadIdx.x == 0) s_qn = 0;
     }
@@ -254,7 +253,7 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
 
 // Owner side of the top-down push: claims (v, parent) received from peers are
 // claimed exactly like local top-down targets (Alg. 2 "(local) ==> (remote)").
-__global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t* __restrict__ off,
+__global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int2* __restrict__ head,
                            uint32_t* __restrict__ visited, int2* __restrict__ out,
                            const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level,
                            int64_t lo) {
@@ -279,10 +278,10 @@ __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int64_t
             base = __shfl_sync(kFull, base, leader);
             if (win) {
                 const int64_t vl = c.x - lo;
-                const int64_t b = off[vl], e = off[vl + 1];
-                queue_put(qnext, base + __popc(m & lanemask_lt()), c.x, b, (int32_t)(e - b));
+                const int32_t dg = __ldg(head + vl).y;
+                queue_put(qnext, base + __popc(m & lanemask_lt()), c.x, dg);
                 out[vl] = make_int2(next_level, c.y);
-                my_mf += (unsigned long long)(e - b);
+                my_mf += (unsigned long long)dg;
             }
         }
     }
@@ -551,8 +550,8 @@ __global__ void k_q2b(const int32_t* __restrict__ q, int64_t F, uint32_t* __rest
     }
 }
 
-// owned slice of a bitmap -> queue of global IDs (with row begin / degree)
-__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, const int64_t* __restrict__ off,
+// owned slice of a bitmap -> queue of global IDs (with degree)
+__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, const int2* __restrict__ head,
                       const Queue q, unsigned long long* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int64_t wbase = lo >> 5;
@@ -576,8 +575,7 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
             const int k = __ffs(bits) - 1;
             bits &= bits - 1;
             const int64_t vl = w * 32 + k;
-            const int64_t b = off[vl], e = off[vl + 1];
-            queue_put(q, pos++, (int32_t)(lo + vl), b, (int32_t)(e - b));
+            queue_put(q, pos++, (int32_t)(lo + vl), __ldg(head + vl).y);
         }
     }
 }
@@ -616,39 +614,53 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
                             const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
                             int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
                             int32_t* __restrict__ parent) {
-    // 4 consecutive original vertices per thread: one 16-byte label load, four
-    // independent lookup/gather chains in flight, 16-byte output stores
+    // kEmitV consecutive original vertices per thread: 16-byte label loads, then the
+    // record gather and the visited lookup of every vertex issued together (the
+    // record of a non-isolated vertex is fetched before knowing whether it was
+    // reached -- in a Kronecker graph nearly all are -- so the chain is label ->
+    // {record, visited} -> store, two dependent hops instead of three).  Internal
+    // labels < n_active have CSR degree > 0, so their skip bit is known to be 0.
+    // Same-degree vertices keep their original order in the reindex (degree desc,
+    // ID asc), so the gathers form one ascending stream per degree value.
+    constexpr int kEmitV = 8;
     const bool vec = ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(parent)) & 15) == 0 &&
                      depth && parent;
-    const int64_t quads = (n + 3) / 4;
-    for (int64_t qd = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; qd < quads; qd += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v0 = qd * 4;
-        int32_t iv[4];
-        if (v0 + 4 <= n) {
-            const int4 l4 = __ldcs(reinterpret_cast<const int4*>(label + v0));
-            iv[0] = l4.x; iv[1] = l4.y; iv[2] = l4.z; iv[3] = l4.w;
+    const int64_t groups = (n + kEmitV - 1) / kEmitV;
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v0 = gi * kEmitV;
+        int32_t iv[kEmitV];
+        if (v0 + kEmitV <= n) {
+#pragma unroll
+            for (int h = 0; h < kEmitV / 4; ++h) {
+                const int4 l4 = __ldcs(reinterpret_cast<const int4*>(label + v0) + h);
+                iv[4 * h] = l4.x; iv[4 * h + 1] = l4.y; iv[4 * h + 2] = l4.z; iv[4 * h + 3] = l4.w;
+            }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) iv[k] = v0 + k < n ? label[v0 + k] : -1;
+            for (int k = 0; k < kEmitV; ++k) iv[k] = v0 + k < n ? label[v0 + k] : -1;
         }
-        uint32_t r[4];
+        int2 o[kEmitV];
+        uint32_t r[kEmitV];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            r[k] = 0;
-            if (iv[k] >= 0 && iv[k] < n_active) r[k] = visited[iv[k] >> 5] & ~skip[iv[k] >> 5];
+        for (int k = 0; k < kEmitV; ++k) {
+            const bool act = iv[k] >= 0 && iv[k] < n_active;
+            o[k] = (act || (iv[k] >= 0 && iv[k] == root_l)) ? __ldg(rec + iv[k]) : make_int2(-1, -1);
+            r[k] = act ? __ldcg(visited + (iv[k] >> 5)) : 0u;
         }
-        int2 o[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            o[k] = make_int2(-1, -1);
-            if (iv[k] >= 0 && (((r[k] >> (iv[k] & 31)) & 1u) || iv[k] == root_l)) o[k] = __ldcs(rec + iv[k]);
-        }
-        if (vec && v0 + 4 <= n) {
-            __stcs(reinterpret_cast<int4*>(depth + v0), make_int4(o[0].x, o[1].x, o[2].x, o[3].x));
-            __stcs(reinterpret_cast<int4*>(parent + v0), make_int4(o[0].y, o[1].y, o[2].y, o[3].y));
+        for (int k = 0; k < kEmitV; ++k)
+            if (!(((r[k] >> (iv[k] & 31)) & 1u) || (iv[k] >= 0 && iv[k] == root_l))) o[k] = make_int2(-1, -1);
+        if (vec && v0 + kEmitV <= n) {
+#pragma unroll
+            for (int h = 0; h < kEmitV / 4; ++h) {
+                __stcs(reinterpret_cast<int4*>(depth + v0) + h,
+                       make_int4(o[4 * h].x, o[4 * h + 1].x, o[4 * h + 2].x, o[4 * h + 3].x));
+                __stcs(reinterpret_cast<int4*>(parent + v0) + h,
+                       make_int4(o[4 * h].y, o[4 * h + 1].y, o[4 * h + 2].y, o[4 * h + 3].y));
+            }
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < kEmitV; ++k) {
                 if (v0 + k >= n) break;
                 if (depth) depth[v0 + k] = o[k].x;
                 if (parent) parent[v0 + k] = o[k].y;
@@ -721,8 +733,6 @@ void bfs_alloc_state(bfs_graph_s* g) {
     g->rec.alloc(qcap, s);
     g->q0.alloc(qcap, s);
     g->q1.alloc(qcap, s);
-    g->qb0.alloc(qcap, s);
-    g->qb1.alloc(qcap, s);
     g->qd0.alloc(qcap, s);
     g->qd1.alloc(qcap, s);
     g->prefix.alloc((size_t)nl + 1, s);
@@ -778,6 +788,15 @@ static void l2_window(bfs_graph_s* g, const void* base, size_t bytes) {
 static void sync_counters(bfs_graph_s* g) {
     cudaStream_t s = g->stream;
     BFS_CUDA(cudaMemcpyAsync(g->cnt.p + C_GLOBAL, g->cnt.p, 8 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
+    if (g->policy.mode == 3) {
+        // the paper's coordinator is partition 0: its local m_f rides along in
+        // the counter allreduce as a slot only rank 0 fills
+        if (!multi(g) || g->comm->rank == 0)
+            BFS_CUDA(cudaMemcpyAsync(g->cnt.p + C_GLOBAL + C_COORD, g->cnt.p + C_MF, sizeof(int64_t),
+                                     cudaMemcpyDeviceToDevice, s));
+        else
+            BFS_CUDA(cudaMemsetAsync(g->cnt.p + C_GLOBAL + C_COORD, 0, sizeof(int64_t), s));
+    }
     if (multi(g)) g->comm->allreduce_sum_i64(g->cnt.p + C_GLOBAL, 8, s);
     BFS_CUDA(cudaMemcpyAsync(g->h_cnt, g->cnt.p, 16 * sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     BFS_CUDA(cudaStreamSynchronize(s));
@@ -843,10 +862,10 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
 
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
     const int64_t pw = padded_words(nl);
-    Queue qcur{g->q0.p, g->qb0.p, g->qd0.p};
-    Queue qnxt{g->q1.p, g->qb1.p, g->qd1.p};
+    Queue qcur{g->q0.p, g->qd0.p};
+    Queue qnxt{g->q1.p, g->qd1.p};
     k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, rec, (int32_t)root, qcur,
-                                             g->off.p, cnt);
+                                             g->head.p, cnt);
     BFS_CHECK_LAUNCH();
     ++launches;
     if (mg) BFS_CUDA(cudaMemsetAsync(g->seen.p, 0, g->seen.bytes(), s));
@@ -860,6 +879,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     int64_t n_f = h[C_GLOBAL + C_NEXT], m_f = h[C_GLOBAL + C_MF];
     int64_t nf_loc = h[C_NEXT], mf_loc = h[C_MF];
     int64_t prev_nf = 0, seen = 0, reached = 0;
+    int64_t m_fc = h[C_GLOBAL + C_COORD], bu_done = 0;  // policy 3: coordinator m_f, BU steps taken
+    bool returned = false;
     const int64_t words = words_of(nl);
     const size_t slice_bytes = mg ? (size_t)(g->nb / 8) : 0;
     uint64_t nvl_total = 0;
@@ -875,6 +896,15 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         switch (g->policy.mode) {
             case 1: dir = 0; break;
             case 2: dir = d >= g->policy.bu_from_level ? 1 : 0; break;
+            case 3:  // the paper's rule (section 3.3; R23)
+                if (dir == 0) {
+                    if (!returned && m_fc * 10000 >= g->policy.alpha * g->arcs_global) dir = 1;
+                } else if (bu_done >= g->policy.beta) {
+                    dir = 0;
+                    returned = true;
+                }
+                if (dir == 1) ++bu_done;
+                break;
             default:
                 if (dir == 0) {
                     if (m_f * g->policy.alpha > m_u) dir = 1;
@@ -890,7 +920,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         if (dir == 0) {
             // ---------------- top-down (Alg. 1, push Alg. 2)
             if (!have_queue) {
-                k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, g->off.p, qcur, cnt);
+                k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, g->head.p, qcur, cnt);
                 BFS_CHECK_LAUNCH();
                 ++launches;
                 have_queue = true;
@@ -916,11 +946,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 const int grid = grid_for(nchunks * kTdThreads, kTdThreads, 8);
                 if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
-                                                                  g->adj.p, g->visited.p, rec, pmap, qnxt, cnt, d + 1,
+                                                                  g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt, d + 1,
                                                                   g->lo, g->hi, rm);
                 else
                     k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
-                                                                   g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, cnt,
+                                                                   g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
                                                                    d + 1, g->lo, g->hi, rm);
                 BFS_CHECK_LAUNCH();
                 launches += 2;
@@ -949,7 +979,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 }
                 g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
                 if (R > 0) {
-                    k_td_merge<<<grid_for(R, 256), 256, 0, s>>>(g->in_list.p, R, g->off.p, g->visited.p, rec, qnxt,
+                    k_td_merge<<<grid_for(R, 256), 256, 0, s>>>(g->in_list.p, R, g->head.p, g->visited.p, rec, qnxt,
                                                                 cnt, d + 1, g->lo);
                     BFS_CHECK_LAUNCH();
                     ++launches;
@@ -1005,6 +1035,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         prev_nf = n_f;
         n_f = h[C_GLOBAL + C_NEXT];
         m_f = h[C_GLOBAL + C_MF];
+        m_fc = h[C_GLOBAL + C_COORD];
         nf_loc = h[C_NEXT];
         mf_loc = h[C_MF];
     }

@@ -135,7 +135,8 @@ struct bfs_graph_s {
     bfsb::DevBuf<int32_t> adj;      // [arcs_local]
     bfsb::DevBuf<int32_t> deg_raw;  // [nl] raw arcs per vertex (TEPS numerator)
     bfsb::DevBuf<uint32_t> skip;    // [padded words of nl] bit set = CSR degree 0
-    bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path
+    bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path,
+                                    // and the degree of a vertex discovered top-down
     bfsb::DevBuf<int32_t> hpar;     // [nl] reindexed only: ORIGINAL label of the first neighbour
     // reindex (identity when absent)
     bool reindexed = false;
@@ -148,7 +149,6 @@ struct bfs_graph_s {
     bfsb::DevBuf<uint32_t> front;    // [padded words of n] global frontier bitmap
     bfsb::DevBuf<uint32_t> next;     // [padded words of n] global next bitmap
     bfsb::DevBuf<int32_t> q0, q1;    // [nl] frontier queues (global internal IDs)
-    bfsb::DevBuf<int64_t> qb0, qb1;  // [nl] row begin of each queued vertex
     bfsb::DevBuf<int32_t> qd0, qd1;  // [nl] degree of each queued vertex
     bfsb::DevBuf<int64_t> prefix;    // [nl + 1] TD degree prefix
     bfsb::DevBuf<int64_t> cnt;       // [8] device counters

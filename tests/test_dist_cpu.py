@@ -47,8 +47,12 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
         dist.all_reduce(t)
         return t.tolist()
 
-    n_f, m_f = allreduce([len(queue), int(sum(deg[v] for v in queue))])
+    def coord(vals):   # mode 3: partition 0 is the coordinator; only it fills the slot
+        return int(sum(deg[v] for v in vals)) if rank == 0 else 0
+
+    n_f, m_f, m_fc = allreduce([len(queue), int(sum(deg[v] for v in queue)), coord(queue)])
     direction, prev, seen_deg, steps = 0, 0, 0, []
+    bu_done, returned = 0, False
     front = np.zeros(p * nb, bool)
     d = 0
     while n_f > 0:
@@ -56,6 +60,13 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
         m_u = ref.arcs - seen_deg
         if mode == 1:
             direction = 0
+        elif mode == 3:
+            if direction == 0:
+                if not returned and m_fc * 10000 >= alpha * ref.arcs:
+                    direction = 1
+            elif bu_done >= beta:
+                direction, returned = 0, True
+            bu_done += direction
         elif direction == 0 and m_f * alpha > m_u:
             direction = 1
         elif direction == 1 and n_f * beta < n and n_f < prev:
@@ -111,9 +122,9 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
                         break
             for v in nxt:
                 visited[v - lo] = True
-        got = allreduce([len(nxt), int(sum(deg[v] for v in nxt)), insp])
+        got = allreduce([len(nxt), int(sum(deg[v] for v in nxt)), insp, coord(nxt)])
         steps.append((direction, n_f, got[0], m_f, m_u, got[2] if direction else m_f))
-        prev, n_f, m_f = n_f, got[0], got[1]
+        prev, n_f, m_f, m_fc = n_f, got[0], got[1], got[3]
         queue = nxt
         d += 1
     return depth, steps
@@ -132,12 +143,12 @@ def _worker(rank, world, port, q):
             lo, hi = pkg.bfs_partition_range(n, world, rank)
             nb = pkg.bfs_partition_range(n, world, 0)[1]
             for root in sorted({0, n - 1, int(np.argmax(g.degree()))}):
-                for mode in (0, 1):
-                    depth, steps = _partitioned_bfs(g, root, lo, hi, nb, world, rank, mode=mode)
+                for mode, alpha, beta in ((0, 15, 18), (1, 15, 18), (3, 500, 2), (3, 40, 3)):
+                    depth, steps = _partitioned_bfs(g, root, lo, hi, nb, world, rank, alpha, beta, mode)
                     full = [None] * world
                     dist.all_gather_object(full, depth.tolist())
                     want, _ = oracle.bfs(g, root)
-                    emu = oracle.do_emulate(g, want, policy=mode)
+                    emu = oracle.do_emulate(g, want, alpha, beta, policy=mode, coord_hi=nb)
                     ok_depth = np.array_equal(np.concatenate(full), want)
                     emu_steps = list(zip(emu["dir"].tolist(), emu["n_f"].tolist(), emu["discovered"].tolist(),
                                          emu["m_f"].tolist(), emu["m_u"].tolist(), emu["insp"].tolist()))

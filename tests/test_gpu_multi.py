@@ -60,7 +60,7 @@ def _check(gs, ref, root, policy, uv=None):
     assert not oracle.validate(ref, int(root), depth, parent, ref_depth=want)
     emu = oracle.do_emulate(ref, want, alpha=policy.get("alpha", 15), beta=policy.get("beta", 18),
                             policy=policy.get("mode", 0), bu_from=policy.get("bu_from_level", 0),
-                            want_bu_parent=True)
+                            want_bu_parent=True, coord_hi=gs[0].local_end)   # coordinator = partition 0
     for lv in levels:   # every rank reports the same global counters
         for key, lk in (("dir", "direction"), ("n_f", "frontier"), ("discovered", "discovered"),
                         ("m_f", "m_f"), ("m_u", "m_u"), ("insp", "inspections")):
@@ -116,7 +116,8 @@ def test_kronecker_s14(p, abc):
     roots = pkg.run_ranks(lambda r: gs[r].sample_roots(scale, seed, 6), p)
     assert all(np.array_equal(roots[0], x) for x in roots)
     assert np.array_equal(roots[0], oracle.sample_roots(ref, scale, seed, 6))
-    pols = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=0, alpha=2, beta=4)]
+    pols = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=0, alpha=2, beta=4),
+            dict(mode=3, alpha=500, beta=3), dict(mode=3, alpha=100, beta=2)]
     for i, r in enumerate(roots[0]):
         runs, levels = _check(gs, ref, r, pols[i % len(pols)], uv)
         if p > 1:
@@ -131,7 +132,7 @@ def test_fixtures_multi(p):
         ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
         comms, gs = _build(p, lambda c, s: pkg.Graph.from_edges(uv, n, comm=c, stream=s))
         for root in sorted({0, n - 1, int(np.argmax(ref.degree()))}):
-            for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
+            for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0), dict(mode=3, alpha=300, beta=2)):
                 _check(gs, ref, root, pol, uv)
         _close(comms, gs)
 

@@ -20,7 +20,8 @@ from paper_1503_04359_b200 import build as pkg_build  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 POLICIES = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=2, bu_from_level=0),
-            dict(mode=0, alpha=2, beta=4), dict(mode=0, alpha=100, beta=2)]
+            dict(mode=0, alpha=2, beta=4), dict(mode=0, alpha=100, beta=2),
+            dict(mode=3, alpha=500, beta=3), dict(mode=3, alpha=50, beta=1)]
 
 
 @pytest.fixture(scope="module", autouse=True)
