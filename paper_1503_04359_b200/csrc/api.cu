@@ -26,6 +26,9 @@ static void (*g_free_fn)(void*, void*) = nullptr;
 static void* g_alloc_ctx = nullptr;
 
 void* dev_alloc(size_t bytes, cudaStream_t s) {
+    // every buffer gets a 16-byte tail: aligned 16-byte vector loads that straddle
+    // the logical end (the bottom-up adjacency reads) stay inside the allocation
+    bytes = (bytes + 31) & ~(size_t)15;
     if (g_alloc_fn) {
         void* p = g_alloc_fn(bytes, (void*)s, g_alloc_ctx);
         if (!p) fail(BFS_ERR_OUT_OF_MEMORY, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");

@@ -219,10 +219,12 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
                 if (lw) {
                     const int64_t vl = v[j] - lo;
                     const int slot = base + __popc(m & lanemask_lt());
-                    const int32_t dg = __ldg(head + vl).y;
+                    // one-shot random accesses stream through L2 with evict-first so the
+                    // visited words the probes and claims hit stay resident
+                    const int32_t dg = __ldcs(head + vl).y;
                     s_q[slot] = v[j];
                     s_qd[slot] = dg;
-                    out[vl] = make_int2(next_level, pmap ? pmap[u[j]] : u[j]);
+                    __stcs(out + vl, make_int2(next_level, pmap ? pmap[u[j]] : u[j]));
                     my_mf += (unsigned long long)dg;
                 }
             }
@@ -293,6 +295,13 @@ __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int
     return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
 
+constexpr int kBuLongDefault = 8;
+// lane-serial probes before a row is handed to the whole warp (BFS_BU_LONG: tuning only)
+static int bu_long_setting() {
+    const char* e = getenv("BFS_BU_LONG");
+    return e ? std::max(1, atoi(e)) : kBuLongDefault;
+}
+
 // Bottom-up step (Alg. 1 BU branch, `break for` P:107, R1).
 // A warp takes a batch of 32 visited words (1024 owned vertices) at a time from a
 // global work counter:
@@ -310,9 +319,9 @@ __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int
 //      hitting lane is the first frontier neighbour in row order);
 //   5. the 32 next words are assembled in shared memory and stored coalesced.
 constexpr int kBuWarps = 8;
-constexpr int kBuSlots = 4;
+constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 4;
-constexpr int kBuLong = 8;
+constexpr int kBuVec = 4;      // arcs a slot reads (one aligned vector load) and probes per round
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
 __global__ void __launch_bounds__(kBuWarps * 32, 4)
@@ -321,7 +330,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
            const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
            const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
            int32_t next_level,
-           unsigned long long* __restrict__ cnt, int grab) {
+           unsigned long long* __restrict__ cnt, int grab, int blong) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
     __shared__ int64_t s_lj[kBuWarps][kLongCap];
@@ -407,7 +416,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             for (int k = 0; k < kBuIlp; ++k) {
                 if (hd[k].y > 0) my_insp += 1;
                 if (hit[k]) {
-                    out[vbase + sv[k]] = make_int2(next_level, po[k]);
+                    __stcs(out + vbase + sv[k], make_int2(next_level, po[k]));
                     atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
                     my_mf += (unsigned long long)hd[k].y;
                 }
@@ -435,8 +444,8 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                 if (t < M) {
                     sv[s] = list[t];
                     t += 32;
-                    sd[s] = __ldg(head + vbase + sv[s]).y;
-                    sj[s] = off[vbase + sv[s]] + 1;
+                    sd[s] = __ldcs(head + vbase + sv[s]).y;
+                    sj[s] = __ldcs(off + vbase + sv[s]) + 1;
                     se[s] = sj[s] - 1 + sd[s];
                     sa[s] = true;
                 }
@@ -446,24 +455,49 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
 #pragma unroll
                 for (int s = 0; s < kBuSlots; ++s) any |= sa[s];
                 if (!__any_sync(kFull, any)) break;
-                int32_t u[kBuSlots];
+                // each slot reads the aligned kBuVec-arc group holding its next arc with
+                // one vector load and probes every arc of it that lies in the row at once
+                int32_t a[kBuSlots][kBuVec];
 #pragma unroll
-                for (int s = 0; s < kBuSlots; ++s) u[s] = sa[s] ? __ldg(adj + sj[s]) : 0;
-                bool h[kBuSlots];
+                for (int s = 0; s < kBuSlots; ++s) {
+                    const int64_t b = sj[s] & ~(int64_t)(kBuVec - 1);
+                    if (kBuVec == 4) {
+                        const int4 x = sa[s] ? __ldg(reinterpret_cast<const int4*>(adj + b)) : make_int4(0, 0, 0, 0);
+                        a[s][0] = x.x; a[s][1] = x.y; a[s][2 % kBuVec] = x.z; a[s][3 % kBuVec] = x.w;
+                    } else if (kBuVec == 2) {
+                        const int2 x = sa[s] ? __ldg(reinterpret_cast<const int2*>(adj + b)) : make_int2(0, 0);
+                        a[s][0] = x.x; a[s][1 % kBuVec] = x.y;
+                    } else {
+                        a[s][0] = sa[s] ? __ldg(adj + b) : 0;
+                    }
+                }
+                bool h[kBuSlots][kBuVec];
 #pragma unroll
-                for (int s = 0; s < kBuSlots; ++s) h[s] = sa[s] && in_front(front, u[s]);
+                for (int s = 0; s < kBuSlots; ++s) {
+                    const int64_t b = sj[s] & ~(int64_t)(kBuVec - 1);
+#pragma unroll
+                    for (int k = 0; k < kBuVec; ++k)
+                        h[s][k] = sa[s] && b + k >= sj[s] && b + k < se[s] && in_front(front, a[s][k]);
+                }
 #pragma unroll
                 for (int s = 0; s < kBuSlots; ++s) {
                     if (sa[s]) {
-                        my_insp += 1;
-                        if (h[s]) {
-                            out[vbase + sv[s]] = make_int2(next_level, pmap ? pmap[u[s]] : u[s]);
+                        const int64_t b = sj[s] & ~(int64_t)(kBuVec - 1);
+                        int kh = -1;
+                        int32_t hu = 0;
+#pragma unroll
+                        for (int k = kBuVec - 1; k >= 0; --k)
+                            if (h[s][k]) { kh = k; hu = a[s][k]; }
+                        const int64_t nj = min(se[s], b + kBuVec);
+                        if (kh >= 0) {
+                            my_insp += (unsigned long long)(b + kh - sj[s] + 1);
+                            __stcs(out + vbase + sv[s], make_int2(next_level, pmap ? pmap[hu] : hu));
                             atomicOr(nbw + (sv[s] >> 5), 1u << (sv[s] & 31));
                             my_mf += (unsigned long long)sd[s];
                             sa[s] = false;
-                        } else if (++sj[s] == se[s]) {
+                        } else if (my_insp += (unsigned long long)(nj - sj[s]), (sj[s] = nj) == se[s]) {
                             sa[s] = false;  // exhausted: no frontier neighbour this level
-                        } else if (sd[s] - (se[s] - sj[s]) >= kBuLong) {
+                        } else if (sd[s] - (se[s] - sj[s]) >= blong) {
                             const int idx = atomicAdd(s_lcount + wid, 1);
                             if (idx < kLongCap) {  // hand the rest of the row to the warp
                                 s_lv[wid][idx] = sv[s];
@@ -477,8 +511,8 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                     if (!sa[s] && t < M) {
                         sv[s] = list[t];
                         t += 32;
-                        sd[s] = __ldg(head + vbase + sv[s]).y;
-                        sj[s] = off[vbase + sv[s]] + 1;
+                        sd[s] = __ldcs(head + vbase + sv[s]).y;
+                        sj[s] = __ldcs(off + vbase + sv[s]) + 1;
                         se[s] = sj[s] - 1 + sd[s];
                         sa[s] = true;
                     }
@@ -623,21 +657,28 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
     // Same-degree vertices keep their original order in the reindex (degree desc,
     // ID asc), so the gathers form one ascending stream per degree value.
     constexpr int kEmitV = 8;
+    // a warp owns a tile of 32 * kEmitV consecutive vertices; part h of the tile is
+    // 128 vertices, lane i holding vertices 4i..4i+3 of it, so every 16-byte label
+    // load and output store of a warp instruction covers 512 contiguous bytes
     const bool vec = ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(parent)) & 15) == 0 &&
                      depth && parent;
-    const int64_t groups = (n + kEmitV - 1) / kEmitV;
-    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < groups; gi += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v0 = gi * kEmitV;
+    const int lane = threadIdx.x & 31;
+    const int64_t tiles = (n + 32 * kEmitV - 1) / (32 * kEmitV);
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tiles; t += nwarps) {
+        const int64_t t0 = t * 32 * kEmitV;
+        const bool full = t0 + 32 * kEmitV <= n;
         int32_t iv[kEmitV];
-        if (v0 + kEmitV <= n) {
 #pragma unroll
-            for (int h = 0; h < kEmitV / 4; ++h) {
-                const int4 l4 = __ldcs(reinterpret_cast<const int4*>(label + v0) + h);
+        for (int h = 0; h < kEmitV / 4; ++h) {
+            const int64_t v0 = t0 + h * 128 + lane * 4;
+            if (full) {
+                const int4 l4 = __ldcs(reinterpret_cast<const int4*>(label + v0));
                 iv[4 * h] = l4.x; iv[4 * h + 1] = l4.y; iv[4 * h + 2] = l4.z; iv[4 * h + 3] = l4.w;
-            }
-        } else {
+            } else {
 #pragma unroll
-            for (int k = 0; k < kEmitV; ++k) iv[k] = v0 + k < n ? label[v0 + k] : -1;
+                for (int j = 0; j < 4; ++j) iv[4 * h + j] = v0 + j < n ? label[v0 + j] : -1;
+            }
         }
         int2 o[kEmitV];
         uint32_t r[kEmitV];
@@ -650,20 +691,21 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
 #pragma unroll
         for (int k = 0; k < kEmitV; ++k)
             if (!(((r[k] >> (iv[k] & 31)) & 1u) || (iv[k] >= 0 && iv[k] == root_l))) o[k] = make_int2(-1, -1);
-        if (vec && v0 + kEmitV <= n) {
 #pragma unroll
-            for (int h = 0; h < kEmitV / 4; ++h) {
-                __stcs(reinterpret_cast<int4*>(depth + v0) + h,
+        for (int h = 0; h < kEmitV / 4; ++h) {
+            const int64_t v0 = t0 + h * 128 + lane * 4;
+            if (vec && full) {
+                __stcs(reinterpret_cast<int4*>(depth + v0),
                        make_int4(o[4 * h].x, o[4 * h + 1].x, o[4 * h + 2].x, o[4 * h + 3].x));
-                __stcs(reinterpret_cast<int4*>(parent + v0) + h,
+                __stcs(reinterpret_cast<int4*>(parent + v0),
                        make_int4(o[4 * h].y, o[4 * h + 1].y, o[4 * h + 2].y, o[4 * h + 3].y));
-            }
-        } else {
+            } else {
 #pragma unroll
-            for (int k = 0; k < kEmitV; ++k) {
-                if (v0 + k >= n) break;
-                if (depth) depth[v0 + k] = o[k].x;
-                if (parent) parent[v0 + k] = o[k].y;
+                for (int j = 0; j < 4; ++j) {
+                    if (v0 + j >= n) break;
+                    if (depth) depth[v0 + j] = o[4 * h + j].x;
+                    if (parent) parent[v0 + j] = o[4 * h + j].y;
+                }
             }
         }
     }
@@ -1010,7 +1052,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
                                                          pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
-                                                         d + 1, cnt, grab);
+                                                         d + 1, cnt, grab, bu_long_setting());
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;
@@ -1044,7 +1086,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     if (od || op) {
         if (g->reindexed) {
             l2_window(g, g->visited.p, g->visited.bytes());
-            k_emit_perm<<<grid_for(g->n, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->n,
+            k_emit_perm<<<grid_for(g->n, 128, 16), 128, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->n,
                                                             g->n_active, root_l, od, op);
         } else {
             k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, nl, root_l, od, op);
