@@ -641,21 +641,16 @@ __global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __r
 
 // Degree-reindexed variant: v runs over ORIGINAL labels and gathers the record of
 // iv = label[v].  Internal labels >= n_active are isolated (the reindex puts them
-// last) and need neither the visited lookup nor the gather.  Everything except the
-// visited bitmap is touched once, so it streams with evict-first hints and the
-// bitmap stays in L2 for the random lookups.
-__global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
-                            const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
+// last) and need no gather unless one is the root.  Labels and outputs are touched
+// once and stream with evict-first hints.
+__global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
                             int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
                             int32_t* __restrict__ parent) {
-    // kEmitV consecutive original vertices per thread: 16-byte label loads, then the
-    // record gather and the visited lookup of every vertex issued together (the
-    // record of a non-isolated vertex is fetched before knowing whether it was
-    // reached -- in a Kronecker graph nearly all are -- so the chain is label ->
-    // {record, visited} -> store, two dependent hops instead of three).  Internal
-    // labels < n_active have CSR degree > 0, so their skip bit is known to be 0.
-    // Same-degree vertices keep their original order in the reindex (degree desc,
-    // ID asc), so the gathers form one ascending stream per degree value.
+    // kEmitV original vertices per thread: 16-byte label loads, then one record
+    // gather per non-isolated vertex (k_mark_unreached has reset the records of the
+    // unreached ones).  Same-degree vertices keep their original order in the
+    // reindex (degree desc, ID asc), so the gathers form one ascending stream per
+    // degree value.
     constexpr int kEmitV = 8;
     // a warp owns a tile of 32 * kEmitV consecutive vertices; part h of the tile is
     // 128 vertices, lane i holding vertices 4i..4i+3 of it, so every 16-byte label
@@ -680,17 +675,14 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
                 for (int j = 0; j < 4; ++j) iv[4 * h + j] = v0 + j < n ? label[v0 + j] : -1;
             }
         }
+        // records of unreached active vertices were reset by k_mark_unreached, so the
+        // record alone decides: no visited lookup
         int2 o[kEmitV];
-        uint32_t r[kEmitV];
 #pragma unroll
         for (int k = 0; k < kEmitV; ++k) {
-            const bool act = iv[k] >= 0 && iv[k] < n_active;
-            o[k] = (act || (iv[k] >= 0 && iv[k] == root_l)) ? __ldg(rec + iv[k]) : make_int2(-1, -1);
-            r[k] = act ? __ldcg(visited + (iv[k] >> 5)) : 0u;
+            const bool act = iv[k] >= 0 && (iv[k] < n_active || iv[k] == root_l);
+            o[k] = act ? __ldg(rec + iv[k]) : make_int2(-1, -1);
         }
-#pragma unroll
-        for (int k = 0; k < kEmitV; ++k)
-            if (!(((r[k] >> (iv[k] & 31)) & 1u) || (iv[k] >= 0 && iv[k] == root_l))) o[k] = make_int2(-1, -1);
 #pragma unroll
         for (int h = 0; h < kEmitV / 4; ++h) {
             const int64_t v0 = t0 + h * 128 + lane * 4;
@@ -707,6 +699,24 @@ __global__ void k_emit_perm(const uint32_t* __restrict__ visited, const uint32_t
                     if (parent) parent[v0 + j] = o[4 * h + j].y;
                 }
             }
+        }
+    }
+}
+
+// rec <- (-1, -1) for every vertex of [0, nbits) with degree > 0 that this search did
+// not reach (a few per search in a Kronecker graph: one coalesced pass over the
+// bitmaps, scattered writes for the unreached only), so that the reindexed output
+// pass can take every active vertex's record as is
+__global__ void k_mark_unreached(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                                 int64_t nbits, int2* __restrict__ rec) {
+    const int64_t words = (nbits + 31) / 32;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t x = ~__ldcs(visited + w) & ~__ldcs(skip + w);
+        if (w == words - 1 && (nbits & 31)) x &= (1u << (nbits & 31)) - 1u;
+        while (x) {
+            const int k = __ffs(x) - 1;
+            x &= x - 1;
+            rec[w * 32 + k] = make_int2(-1, -1);
         }
     }
 }
@@ -1085,8 +1095,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
     if (od || op) {
         if (g->reindexed) {
-            l2_window(g, g->visited.p, g->visited.bytes());
-            k_emit_perm<<<grid_for(g->n, 128, 16), 128, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->n,
+            k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
+                                                                                   rec);
+            BFS_CHECK_LAUNCH();
+            ++launches;
+            k_emit_perm<<<grid_for(g->n, 128, 16), 128, 0, s>>>(rec, g->label.p, g->n,
                                                             g->n_active, root_l, od, op);
         } else {
             k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, nl, root_l, od, op);
