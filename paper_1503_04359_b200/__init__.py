@@ -53,7 +53,7 @@ class bfs_build_opts(ctypes.Structure):
 
 class bfs_policy(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("alpha", ctypes.c_int64), ("beta", ctypes.c_int64),
-                ("bu_from_level", ctypes.c_int), ("level_times", ctypes.c_int)]
+                ("bu_from_level", ctypes.c_int), ("level_times", ctypes.c_int), ("host_loop", ctypes.c_int)]
 
 
 class bfs_level_stats(ctypes.Structure):
@@ -193,8 +193,9 @@ def bfs_graph_build_ms(h) -> float:
     return x.value
 
 
-def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_level: int = 0, level_times: bool = False):
-    p = bfs_policy(mode, alpha, beta, bu_from_level, int(level_times))
+def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_level: int = 0, level_times: bool = False,
+                   host_loop: bool = False):
+    p = bfs_policy(mode, alpha, beta, bu_from_level, int(level_times), int(host_loop))
     _check(lib().bfs_set_policy(h, ctypes.byref(p)))
 
 
@@ -208,8 +209,12 @@ def bfs_component_tuples(h) -> int:
     return t.value
 
 
-def bfs_stats(h, max_levels: int = 64):
+def bfs_stats(h, max_levels: int | None = None):
+    """(run, levels) of the last search; every step record unless max_levels caps it."""
     rs = bfs_run_stats()
+    if max_levels is None:
+        _check(lib().bfs_stats(h, ctypes.byref(rs), None, 0))
+        max_levels = max(1, rs.levels)
     lv = (bfs_level_stats * max_levels)()
     _check(lib().bfs_stats(h, ctypes.byref(rs), lv, max_levels))
     levels = [{f: getattr(lv[i], f) for f, _ in bfs_level_stats._fields_} for i in range(min(rs.levels, max_levels))]

@@ -286,6 +286,7 @@ bfs_status bfs_set_policy(bfs_graph_t g, const bfs_policy* p) {
     if (p->alpha < 1 || p->alpha > (1 << 24) || p->beta < 1 || p->beta > (1 << 24))
         fail(BFS_ERR_INVALID_ARG, "alpha and beta must be in [1, 2^24]");
     if (p->bu_from_level < 0) fail(BFS_ERR_INVALID_ARG, "bu_from_level must be >= 0");
+    if (p->host_loop < 0 || p->host_loop > 1) fail(BFS_ERR_INVALID_ARG, "host_loop must be 0 or 1");
     g->policy = *p;
     API_END
 }
@@ -329,6 +330,8 @@ bfs_status bfs_graph_destroy(bfs_graph_t g) {
         if (e) cudaEventDestroy(e);
     for (auto& e : g->lev_ev) cudaEventDestroy(e);
     if (g->h_cnt) cudaFreeHost(g->h_cnt);
+    if (g->h_cnt_mat) cudaFreeHost(g->h_cnt_mat);
+    bfsb::bfs_release_loop(g);
     delete g;
     cudaDeviceSynchronize();
     API_END

@@ -28,6 +28,10 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <tuple>
+#include <type_traits>
+#include <utility>
+#include <vector>
 
 #include "internal.cuh"
 
@@ -69,6 +73,38 @@ __device__ __forceinline__ void queue_put(const Queue& q, unsigned long long pos
     __stcs(q.deg + pos, deg);
 }
 
+// Device-resident state of the device-driven level loop (one GPU).  The
+// step kernels read their sizes and buffer selectors from here when launched from
+// the loop graph, and take them by value (ctl == nullptr) from the host loop.
+struct Ctl {
+    long long n_f, m_f, prev_nf, seen, reached, m_fc;
+    long long E, nchunks;     // top-down sizes of the current step
+    long long root_i;         // internal label of the root
+    long long alpha, beta, n, arcs;
+    int d, dir, have_queue, qsel, fsel, bu_done, returned, overflow;
+    int mode, bu_from, max_levels, pad;
+};
+// one record per step, filled by the step kernels (times: %globaltimer ns)
+struct LevelRec {
+    long long n_f, discovered, m_f, m_u, insp, scanned;
+    unsigned long long ts, te, k0, k1;   // step begin / end; main kernel first block start / last block end
+    int dir, pad;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// main-kernel span: first block start / last block end into the step's record
+__device__ __forceinline__ void stamp_begin(LevelRec* lrec, const Ctl* ctl) {
+    if (lrec && threadIdx.x == 0) atomicMin(&lrec[ctl->d].k0, gtimer());
+}
+__device__ __forceinline__ void stamp_end(LevelRec* lrec, const Ctl* ctl) {
+    if (lrec && threadIdx.x == 0) atomicMax(&lrec[ctl->d].k1, gtimer());
+}
+
 // root_l < 0 on ranks that do not own the root
 __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int64_t root_l, int32_t root_g,
                        int2* out, int32_t root_o, Queue q, const int2* head, unsigned long long* cnt) {
@@ -90,7 +126,12 @@ __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int6
 }
 
 // chunk c of the top-down arc range starts inside frontier entry starts[c]
-__global__ void k_td_chunk_starts(const int64_t* prefix, int64_t F, int64_t nchunks, int64_t* starts) {
+__global__ void k_td_chunk_starts(const int64_t* prefix, int64_t F, int64_t nchunks, int64_t* starts,
+                                  const Ctl* ctl) {
+    if (ctl) {
+        F = ctl->n_f;
+        nchunks = ctl->nchunks;
+    }
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = c * kTdChunk;
         // largest i in [0, F) with prefix[i] <= e (prefix non-decreasing, prefix[0] = 0)
@@ -121,11 +162,11 @@ struct Remote {          // p > 1 only
 //      CTA chunk on the global queue tail, then a coalesced copy of the stage.
 template <bool kMulti>
 __global__ void __launch_bounds__(kTdThreads)
-k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
+k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
-            const Queue qnext, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
-            int32_t next_level, int64_t lo, int64_t hi, Remote rm) {
+            const Queue qnext_in, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
+            int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec) {
     __shared__ int64_t s_pre[kTdChunk + 2];
     __shared__ int64_t s_beg[kTdChunk + 1];
     __shared__ int32_t s_u[kTdChunk + 1];
@@ -135,6 +176,15 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
     __shared__ unsigned long long s_base;
     const int lane = threadIdx.x & 31;
     unsigned long long my_mf = 0;
+    Queue qc = q_in, qnext = qnext_in;
+    if (ctl) {   // device-driven loop: sizes and queue selector from the loop state
+        F = ctl->n_f;
+        E = ctl->E;
+        next_level = ctl->d + 1;
+        if (ctl->qsel) { qc = qnext_in; qnext = q_in; }
+        stamp_begin(lrec, ctl);
+    }
+    const Queue q = qc;
     const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
     if (threadIdx.x == 0) s_qn = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -251,6 +301,10 @@ k_td_expand(const Queue q, const int64_t* __restrict__ prefix, const int64_t* __
     }
     my_mf = warp_sum_u64(my_mf);
     if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+    if (ctl && lrec) {
+        __syncthreads();
+        stamp_end(lrec, ctl);
+    }
 }
 
 // Owner side of the top-down push: claims (v, parent) received from peers are
@@ -327,10 +381,10 @@ constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (
 __global__ void __launch_bounds__(kBuWarps * 32, 4)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
-           const uint32_t* __restrict__ front, uint32_t* __restrict__ next, int2* __restrict__ out,
+           const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
            const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
            int32_t next_level,
-           unsigned long long* __restrict__ cnt, int grab, int blong) {
+           unsigned long long* __restrict__ cnt, int grab, int blong, const Ctl* ctl, LevelRec* lrec) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
     __shared__ int64_t s_lj[kBuWarps][kLongCap];
@@ -339,6 +393,16 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
     __shared__ int32_t s_ld[kBuWarps][kLongCap];
     __shared__ int s_lcount[kBuWarps];
     const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t* front = front_in;
+    uint32_t* next = next_in;
+    if (ctl) {   // device-driven loop: the bitmap pair flips every bottom-up step
+        next_level = ctl->d + 1;
+        if (ctl->fsel) {
+            front = next_in;
+            next = const_cast<uint32_t*>(front_in);
+        }
+        stamp_begin(lrec, ctl);
+    }
     uint16_t* list = s_list[wid];
     uint32_t* nbw = s_nb[wid];
     const int64_t wbase = lo >> 5;
@@ -574,19 +638,25 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
         if (my_insp) atomicAdd(cnt + C_INSP, my_insp);
         if (my_scan) atomicAdd(cnt + C_SCAN, my_scan);
     }
+    if (ctl && lrec) {
+        __syncthreads();
+        stamp_end(lrec, ctl);
+    }
 }
 
 // queue -> bitmap (the owned slice of front is cleared beforehand)
-__global__ void k_q2b(const int32_t* __restrict__ q, int64_t F, uint32_t* __restrict__ front) {
+__device__ __forceinline__ void q2b_body(const int32_t* __restrict__ q, int64_t F, uint32_t* __restrict__ front) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < F; i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t v = q[i];
         atomicOr(front + (v >> 5), 1u << (v & 31));
     }
 }
+__global__ void k_q2b(const int32_t* __restrict__ q, int64_t F, uint32_t* __restrict__ front) { q2b_body(q, F, front); }
 
 // owned slice of a bitmap -> queue of global IDs (with degree)
-__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, const int2* __restrict__ head,
-                      const Queue q, unsigned long long* __restrict__ cnt) {
+__device__ __forceinline__ void b2q_body(const uint32_t* __restrict__ bm, int64_t words, int64_t lo,
+                                         const int2* __restrict__ head, const Queue q,
+                                         unsigned long long* __restrict__ cnt) {
     const int lane = threadIdx.x & 31;
     const int64_t wbase = lo >> 5;
     for (int64_t b0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; b0 < words;
@@ -614,6 +684,11 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
     }
 }
 
+__global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo, const int2* __restrict__ head,
+                      const Queue q, unsigned long long* __restrict__ cnt) {
+    b2q_body(bm, words, lo, head, q, cnt);
+}
+
 // Output pass (the only writer of the caller's arrays): every entry of depth and
 // parent is written exactly once, in order, with full coalesced lines.  During
 // the traversal the steps record (depth, parent) of each discovered vertex as one
@@ -628,7 +703,8 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
 // bitmap stays in L2 for the random lookups.
 __global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
                        const int2* __restrict__ rec, int64_t nl, int64_t root_l, int32_t* __restrict__ depth,
-                       int32_t* __restrict__ parent) {
+                       int32_t* __restrict__ parent, const Ctl* ctl) {
+    if (ctl) root_l = ctl->root_i;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = v >> 5;
         const uint32_t r = visited[w] & ~skip[w];
@@ -645,7 +721,8 @@ __global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __r
 // once and stream with evict-first hints.
 __global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
                             int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
-                            int32_t* __restrict__ parent) {
+                            int32_t* __restrict__ parent, const Ctl* ctl) {
+    if (ctl) root_l = ctl->root_i;
     // kEmitV original vertices per thread: 16-byte label loads, then one record
     // gather per non-isolated vertex (k_mark_unreached has reset the records of the
     // unreached ones).  Same-degree vertices keep their original order in the
@@ -760,6 +837,218 @@ __global__ void k_gather_labels(const int32_t* __restrict__ label, const int32_t
         out[i] = in[i] < 0 ? -1 : label[in[i]];
 }
 
+// ============================================================ device-driven level loop
+// (SURVEY f3).  On one GPU the whole level loop is one CUDA graph: a WHILE node
+// whose body is k_step_begin (the alpha/beta decision, on the device) -> IF(top-down)
+// {k_td_prep -> k_scan_dev -> k_td_chunk_starts -> k_td_expand} and IF(bottom-up)
+// {k_bu_prep -> k_q2b_dev -> k_bu_batch} -> k_step_end (roll the counters, record
+// the step, continue while the frontier is non-empty).  The host launches it once
+// per search and synchronises once, instead of once per level.
+
+// init on the device: the root's internal label, visited <- skip | root, root
+// record, the first queue, the loop state (policy included)
+__global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip, int64_t pw,
+                           int64_t root, const int32_t* __restrict__ label, int2* __restrict__ out, Queue q,
+                           const int2* __restrict__ head, unsigned long long* __restrict__ cnt, Ctl* ctl,
+                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels) {
+    const int64_t ri = label ? (int64_t)__ldg(label + root) : root;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t x = skip[w];
+        if (w == (ri >> 5)) x |= 1u << (ri & 31);
+        visited[w] = x;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (int i = 0; i < 16; ++i) cnt[i] = 0;
+        out[ri] = make_int2(0, (int32_t)root);
+        const int32_t dg = head[ri].y;
+        queue_put(q, 0, (int32_t)ri, dg);
+        Ctl c{};
+        c.n_f = 1;
+        c.m_f = c.m_fc = dg;
+        c.root_i = ri;
+        c.alpha = pol.alpha;
+        c.beta = pol.beta;
+        c.n = n;
+        c.arcs = arcs;
+        c.have_queue = 1;
+        c.mode = pol.mode;
+        c.bu_from = pol.bu_from_level;
+        c.max_levels = max_levels;
+        *ctl = c;
+    }
+}
+
+__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_td,
+                             cudaGraphConditionalHandle h_bu) {
+    Ctl c = *ctl;
+    const long long t = gtimer();
+    c.reached += c.n_f;
+    c.seen += c.m_f;
+    const long long m_u = c.arcs - c.seen;
+    // direction for the step that builds level d+1: the host loop's rule, verbatim
+    switch (c.mode) {
+        case 1: c.dir = 0; break;
+        case 2: c.dir = c.d >= c.bu_from ? 1 : 0; break;
+        case 3:
+            if (c.dir == 0) {
+                if (!c.returned && c.m_fc * 10000 >= c.alpha * c.arcs) c.dir = 1;
+            } else if (c.bu_done >= c.beta) {
+                c.dir = 0;
+                c.returned = 1;
+            }
+            if (c.dir == 1) ++c.bu_done;
+            break;
+        default:
+            if (c.dir == 0) {
+                if (c.m_f * c.alpha > m_u) c.dir = 1;
+            } else {
+                if (c.n_f * c.beta < c.n && c.n_f < c.prev_nf) c.dir = 0;
+            }
+    }
+    c.E = c.m_f;
+    c.nchunks = (c.E + kTdChunk - 1) / kTdChunk;
+    LevelRec r{};
+    r.n_f = c.n_f;
+    r.m_f = c.m_f;
+    r.m_u = m_u;
+    r.dir = c.dir;
+    r.ts = t;
+    r.k0 = ~0ull;
+    lrec[c.d] = r;
+    for (int i = 0; i < 8; ++i) cnt[i] = 0;
+    *ctl = c;
+    cudaGraphSetConditional(h_td, c.dir == 0 ? 1u : 0u);
+    cudaGraphSetConditional(h_bu, c.dir == 1 ? 1u : 0u);
+}
+
+__global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* cnt, cudaGraphConditionalHandle h_loop) {
+    Ctl c = *ctl;
+    LevelRec& r = lrec[c.d];
+    const long long next = (long long)cnt[C_NEXT], mf = (long long)cnt[C_MF];
+    r.discovered = next;
+    r.insp = c.dir == 0 ? c.m_f : (long long)cnt[C_INSP];
+    r.scanned = c.dir == 0 ? c.n_f : (long long)cnt[C_SCAN];
+    r.te = gtimer();
+    if (c.dir == 0) {
+        c.qsel ^= 1;
+        c.have_queue = 1;
+    } else {
+        c.fsel ^= 1;
+        c.have_queue = 0;
+    }
+    c.prev_nf = c.n_f;
+    c.n_f = next;
+    c.m_f = c.m_fc = mf;
+    c.d += 1;
+    int cont = next > 0;
+    if (cont && c.d >= c.max_levels) {
+        c.overflow = 1;
+        cont = 0;
+    }
+    *ctl = c;
+    cudaGraphSetConditional(h_loop, (unsigned)cont);
+}
+
+// top-down prologue: frontier bitmap -> queue when the previous step was bottom-up,
+// and a fresh tile state for the single-pass scan
+__global__ void k_td_prep(const Ctl* ctl, const uint32_t* __restrict__ f0, const uint32_t* __restrict__ f1,
+                          int64_t words, const int2* __restrict__ head, Queue qa, Queue qb,
+                          unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ tstate,
+                          unsigned int* __restrict__ tctr) {
+    const int64_t tiles = (ctl->n_f + 2047) / 2048;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tiles; i += (int64_t)gridDim.x * blockDim.x)
+        tstate[i] = 0ull;
+    if (blockIdx.x == 0 && threadIdx.x == 0) *tctr = 0u;
+    if (!ctl->have_queue) b2q_body(ctl->fsel ? f1 : f0, words, 0, head, ctl->qsel ? qb : qa, cnt);
+}
+
+// Single-pass exclusive scan of the current queue's degrees (decoupled look-back:
+// tiles are taken in order from a counter, each publishes its aggregate, then its
+// inclusive prefix once the look-back over its predecessors resolves).  n+1 outputs.
+constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
+constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue qa, Queue qb, int64_t* __restrict__ out,
+                                                           unsigned long long* tstate, unsigned int* tctr) {
+    __shared__ long long s_tile, s_excl;
+    __shared__ long long s_warp[kScanThreads / 32];
+    const long long n = ctl->n_f;
+    const int32_t* __restrict__ deg = ctl->qsel ? qb.deg : qa.deg;
+    const long long tiles = (n + kScanTile - 1) / kScanTile;
+    if (n == 0) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
+        return;
+    }
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_tile = atomicAdd(tctr, 1u);
+        __syncthreads();
+        const long long t = s_tile;
+        if (t >= tiles) break;
+        const long long base = t * kScanTile + (long long)threadIdx.x * kScanItems;
+        long long v[kScanItems], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            v[k] = base + k < n ? (long long)deg[base + k] : 0;
+            sum += v[k];
+        }
+        long long inc = sum;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const long long y = __shfl_up_sync(kFull, inc, dd);
+            if (lane >= dd) inc += y;
+        }
+        if (lane == 31) s_warp[wid] = inc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            long long run = 0;
+            for (int w = 0; w < kScanThreads / 32; ++w) {
+                const long long x = s_warp[w];
+                s_warp[w] = run;
+                run += x;
+            }
+            const long long agg = run;
+            long long excl = 0;
+            volatile unsigned long long* st = tstate;
+            if (t == 0) {
+                st[0] = kFlagP | (unsigned long long)agg;
+            } else {
+                st[t] = kFlagA | (unsigned long long)agg;
+                for (long long j = t - 1; j >= 0;) {
+                    const unsigned long long x = st[j];
+                    if (!(x >> 62)) continue;   // predecessor not published yet
+                    excl += (long long)(x & kValMask);
+                    if ((x >> 62) == 2) break;
+                    --j;
+                }
+                st[t] = kFlagP | (unsigned long long)(excl + agg);
+            }
+            s_excl = excl;
+            if (t == tiles - 1) out[n] = excl + agg;
+        }
+        __syncthreads();
+        long long pre = s_excl + s_warp[wid] + inc - sum;
+#pragma unroll
+        for (int k = 0; k < kScanItems; ++k) {
+            if (base + k < n) out[base + k] = pre;
+            pre += v[k];
+        }
+        __syncthreads();
+    }
+}
+
+// bottom-up prologue: queue -> bitmap when the previous step was top-down (clear, then set)
+__global__ void k_bu_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1, int64_t words) {
+    if (!ctl->have_queue) return;
+    uint32_t* f = ctl->fsel ? f1 : f0;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+        f[w] = 0u;
+}
+__global__ void k_q2b_dev(const Ctl* ctl, Queue qa, Queue qb, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1) {
+    if (!ctl->have_queue) return;
+    q2b_body((ctl->qsel ? qb : qa).v, ctl->n_f, ctl->fsel ? f1 : f0);
+}
+
 int grid_for(int64_t items, int threads, int per_sm = 8) {
     const int64_t b = (items + threads - 1) / threads;
     const int64_t cap = (int64_t)num_sms() * per_sm;
@@ -862,6 +1151,192 @@ static void ensure(DevBuf<T>& b, size_t count, cudaStream_t s) {
     }
 }
 
+// ---------------------------------------------------------------- the loop graph
+constexpr int kGraphMaxLevels = 4096;   // deeper searches fall back to the host loop
+constexpr int kLrecHead = 64;           // records read back with the state in one copy
+static_assert(sizeof(Ctl) % 8 == 0 && sizeof(LevelRec) % 8 == 0, "8-byte records");
+
+template <class... P, class... A>
+static cudaGraphNode_t add_kernel(cudaGraph_t G, const std::vector<cudaGraphNode_t>& deps, void (*fn)(P...), dim3 grid,
+                                  dim3 block, size_t smem, A&&... args) {
+    static_assert(sizeof...(P) == sizeof...(A), "argument count");
+    std::tuple<std::decay_t<P>...> t(std::forward<A>(args)...);
+    void* ptrs[sizeof...(P)];
+    std::apply([&](auto&... x) {
+        int i = 0;
+        ((ptrs[i++] = (void*)&x), ...);
+    }, t);
+    cudaKernelNodeParams kp{};
+    kp.func = (void*)fn;
+    kp.gridDim = grid;
+    kp.blockDim = block;
+    kp.sharedMemBytes = (unsigned)smem;
+    kp.kernelParams = ptrs;
+    cudaGraphNode_t n;
+    BFS_CUDA(cudaGraphAddKernelNode(&n, G, deps.data(), deps.size(), &kp));
+    return n;
+}
+
+static cudaGraph_t add_cond(cudaGraph_t G, const std::vector<cudaGraphNode_t>& deps, cudaGraphConditionalHandle h,
+                            cudaGraphConditionalNodeType type, cudaGraphNode_t* node) {
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = type;
+    cp.conditional.size = 1;
+    BFS_CUDA(cudaGraphAddNode(node, G, deps.data(), deps.size(), &cp));
+    return cp.conditional.phGraph_out[0];
+}
+
+static void build_loop_graph(bfs_graph_s* g) {
+    cudaStream_t s = g->stream;
+    const int64_t nl = g->nl();
+    const int64_t words = words_of(nl);
+    if (!g->ctl.p) {
+        g->ctl.alloc(sizeof(Ctl) / 8, s);
+        g->lrec.alloc((size_t)kGraphMaxLevels * sizeof(LevelRec) / 8, s);
+        g->tstate.alloc((size_t)(nl / kScanTile + 2), s);
+        g->tctr.alloc(1, s);
+        BFS_CUDA(cudaMallocHost(&g->h_ctl, sizeof(Ctl) + kLrecHead * sizeof(LevelRec)));
+        BFS_CUDA(cudaMallocHost(&g->h_lrec, (size_t)kGraphMaxLevels * sizeof(LevelRec)));
+    }
+    Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
+    LevelRec* lrec = reinterpret_cast<LevelRec*>(g->lrec.p);
+    unsigned long long* cnt = (unsigned long long*)g->cnt.p;
+    unsigned long long* tstate = (unsigned long long*)g->tstate.p;
+    const Queue qa{g->q0.p, g->qd0.p}, qb{g->q1.p, g->qd1.p};
+    const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
+    const int sms = num_sms();
+    const dim3 g8(sms * 8), t256(256);
+
+    cudaGraph_t G;
+    BFS_CUDA(cudaGraphCreate(&G, 0));
+    cudaGraphConditionalHandle h_loop, h_td, h_bu;
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_loop, G, 1, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_while, n_td, n_bu;
+    cudaGraph_t B = add_cond(G, {}, h_loop, cudaGraphCondTypeWhile, &n_while);
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_td, B, 0, cudaGraphCondAssignDefault));
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_bu, B, 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step_begin, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_td, h_bu);
+    cudaGraph_t T = add_cond(B, {n_begin}, h_td, cudaGraphCondTypeIf, &n_td);
+    cudaGraph_t U = add_cond(B, {n_begin}, h_bu, cudaGraphCondTypeIf, &n_bu);
+    add_kernel(B, {n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
+    // top-down body
+    cudaGraphNode_t t1 = add_kernel(T, {}, k_td_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words, g->head.p, qa, qb,
+                                    cnt, tstate, g->tctr.p);
+    cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, g->prefix.p, tstate,
+                                    g->tctr.p);
+    cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
+                                    g->scratch64.p, ctl);
+    add_kernel(T, {t3}, k_td_expand<false>, g8, dim3(kTdThreads), 0, qa, g->prefix.p, g->scratch64.p, (int64_t)0,
+               (int64_t)0, g->off.p, g->adj.p, g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo,
+               g->hi, Remote{}, ctl, lrec);
+    // bottom-up body
+    cudaGraphNode_t u1 = add_kernel(U, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
+    cudaGraphNode_t u2 = add_kernel(U, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
+    const int64_t nbatches = (words + 31) / 32;
+    const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, 4);
+    const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
+    add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
+               g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
+               cnt, grab, bu_long_setting(), ctl, lrec);
+    BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
+    g->loop_graph = G;
+}
+
+void bfs_release_loop(bfs_graph_s* g) {
+    if (g->loop_exec) cudaGraphExecDestroy(g->loop_exec);
+    if (g->loop_graph) cudaGraphDestroy(g->loop_graph);
+    if (g->h_ctl) cudaFreeHost(g->h_ctl);
+    if (g->h_lrec) cudaFreeHost(g->h_lrec);
+    g->loop_exec = nullptr;
+    g->loop_graph = nullptr;
+    g->h_ctl = g->h_lrec = nullptr;
+}
+
+// One search with the device-driven loop.  Returns false (nothing to report) if
+// the search ran past kGraphMaxLevels levels; the caller reruns it host-driven.
+static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op, int32_t* parent_out,
+                          int32_t* depth_out) {
+    cudaStream_t s = g->stream;
+    const int64_t nl = g->nl();
+    if (!g->loop_exec) build_loop_graph(g);
+    Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
+    const Queue qa{g->q0.p, g->qd0.p};
+    const int64_t pw = padded_words(nl);
+    const bool lt = g->policy.level_times != 0;
+    BFS_CUDA(cudaEventRecord(g->ev[0], s));
+    k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
+                                                 g->rec.p, qa, g->head.p, (unsigned long long*)g->cnt.p, ctl, g->policy,
+                                                 g->n, g->arcs_global, kGraphMaxLevels);
+    BFS_CHECK_LAUNCH();
+    BFS_CUDA(cudaEventRecord(g->ev[2], s));
+    BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
+    BFS_CUDA(cudaEventRecord(g->ev[3], s));
+    int64_t launches = 1;
+    if (od || op) {
+        if (g->reindexed) {
+            k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
+                                                                                   g->rec.p);
+            BFS_CHECK_LAUNCH();
+            k_emit_perm<<<grid_for(g->n, 128, 16), 128, 0, s>>>(g->rec.p, g->label.p, g->n, g->n_active, 0, od, op, ctl);
+            launches += 2;
+        } else {
+            k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->rec.p, nl, 0, od, op, ctl);
+            launches += 1;
+        }
+        BFS_CHECK_LAUNCH();
+    }
+    BFS_CUDA(cudaEventRecord(g->ev[1], s));
+    if (depth_out && od != depth_out) BFS_CUDA(cudaMemcpyAsync(depth_out, od, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
+    if (parent_out && op != parent_out)
+        BFS_CUDA(cudaMemcpyAsync(parent_out, op, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
+    // the one read-back of the search: loop state plus the first kLrecHead step records
+    BFS_CUDA(cudaMemcpyAsync(g->h_ctl, g->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaMemcpyAsync(g->h_lrec, g->lrec.p, kLrecHead * sizeof(LevelRec), cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaStreamSynchronize(s));
+    const Ctl c = *reinterpret_cast<const Ctl*>(g->h_ctl);
+    if (c.overflow) return false;
+    if (c.d > kLrecHead) {
+        BFS_CUDA(cudaMemcpyAsync(g->h_lrec + kLrecHead * sizeof(LevelRec) / 8, g->lrec.p + kLrecHead * sizeof(LevelRec) / 8,
+                                 (size_t)(c.d - kLrecHead) * sizeof(LevelRec), cudaMemcpyDeviceToHost, s));
+        BFS_CUDA(cudaStreamSynchronize(s));
+    }
+    const LevelRec* R = reinterpret_cast<const LevelRec*>(g->h_lrec);
+    double comp = 0;
+    for (int d = 0; d < c.d; ++d) {
+        bfs_level_stats L{};
+        L.level = d;
+        L.direction = R[d].dir;
+        L.frontier = R[d].n_f;
+        L.discovered = R[d].discovered;
+        L.m_f = R[d].m_f;
+        L.m_u = R[d].m_u;
+        L.inspections = R[d].insp;
+        L.scanned = R[d].scanned;
+        if (lt) {
+            L.ms = (float)((double)(R[d].te - R[d].ts) * 1e-6);
+            L.kernel_ms = R[d].k1 > R[d].k0 ? (float)((double)(R[d].k1 - R[d].k0) * 1e-6) : 0.f;
+            comp += L.kernel_ms;
+        }
+        g->levels.push_back(L);
+        launches += 2 + (R[d].dir == 0 ? 4 : 3);
+    }
+    float ms = 0, ms_init = 0, ms_loop = 0;
+    BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
+    BFS_CUDA(cudaEventElapsedTime(&ms_init, g->ev[0], g->ev[2]));
+    BFS_CUDA(cudaEventElapsedTime(&ms_loop, g->ev[2], g->ev[3]));
+    g->run.ms_total = ms;
+    g->run.ms_init = ms_init;
+    g->run.ms_compute = lt ? comp : ms_loop;
+    g->run.levels = c.d;
+    g->run.reached = c.reached;
+    g->run.kernel_launches = launches;
+    g->last_root_l = c.root_i;
+    g->run.component_edge_tuples = -1;
+    return true;
+}
+
 void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out) {
     if (root < 0 || root >= g->n)
         fail(BFS_ERR_OUT_OF_RANGE, "root " + std::to_string(root) + " outside [0, " + std::to_string(g->n) + ")");
@@ -872,15 +1347,6 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     const int me = mg ? g->comm->rank : 0;
     unsigned long long* cnt = (unsigned long long*)g->cnt.p;
     int64_t* h = g->h_cnt;
-
-    int64_t root_i = root;
-    if (g->reindexed) {
-        int32_t r;
-        BFS_CUDA(cudaMemcpy(&r, g->label.p + root, sizeof(int32_t), cudaMemcpyDeviceToHost));
-        root_i = r;
-    }
-    const bool own_root = root_i >= g->lo && root_i < g->hi;
-    const int64_t root_l = own_root ? root_i - g->lo : -1;
 
     // the steps record (depth, parent) per discovered vertex in `rec` (internal
     // order); k_emit writes the caller's arrays (device) or staging buffers (host)
@@ -902,6 +1368,26 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     g->levels.clear();
     g->run = bfs_run_stats{};
     g->run.root = root;
+    static const bool env_host_loop = [] {
+        const char* e = getenv("BFS_HOST_LOOP");   // A/B experiments only
+        return e && e[0] == '1';
+    }();
+    if (!mg && g->nparts == 1 && !g->policy.host_loop && !env_host_loop) {
+        if (bfs_run_graph(g, root, od, op, parent_out, depth_out)) return;
+        g->levels.clear();   // deeper than the graph's record capacity: host loop below
+        g->run = bfs_run_stats{};
+        g->run.root = root;
+    }
+    // ---------------- host-driven level loop (p ranks, or policy.host_loop)
+    int64_t root_i = root;
+    if (g->reindexed) {
+        int32_t r;
+        BFS_CUDA(cudaMemcpy(&r, g->label.p + root, sizeof(int32_t), cudaMemcpyDeviceToHost));
+        root_i = r;
+    }
+    const bool own_root = root_i >= g->lo && root_i < g->hi;
+    const int64_t root_l = own_root ? root_i - g->lo : -1;
+
     int64_t launches = 0;
     // per-step events: [4d] step start, [4d+1] main kernel start, [4d+2] main kernel end,
     // [4d+3] exchange end (p > 1)
@@ -993,17 +1479,18 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 l2_window(g, g->visited.p, g->visited.bytes());
                 launches += scan_exclusive_i32(qcur.deg, g->prefix.p, nf_loc, s);
                 const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
-                k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p);
+                k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p,
+                                                                          nullptr);
                 BFS_CHECK_LAUNCH();
                 const int grid = grid_for(nchunks * kTdThreads, kTdThreads, 8);
                 if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
                                                                   g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt, d + 1,
-                                                                  g->lo, g->hi, rm);
+                                                                  g->lo, g->hi, rm, nullptr, nullptr);
                 else
                     k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
                                                                    g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
-                                                                   d + 1, g->lo, g->hi, rm);
+                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr);
                 BFS_CHECK_LAUNCH();
                 launches += 2;
             }
@@ -1062,7 +1549,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
                                                          pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
-                                                         d + 1, cnt, grab, bu_long_setting());
+                                                         d + 1, cnt, grab, bu_long_setting(), nullptr,
+                                                         nullptr);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
             ++launches;
@@ -1100,9 +1588,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             BFS_CHECK_LAUNCH();
             ++launches;
             k_emit_perm<<<grid_for(g->n, 128, 16), 128, 0, s>>>(rec, g->label.p, g->n,
-                                                            g->n_active, root_l, od, op);
+                                                            g->n_active, root_l, od, op, nullptr);
         } else {
-            k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, nl, root_l, od, op);
+            k_emit<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, nl, root_l, od, op, nullptr);
         }
         BFS_CHECK_LAUNCH();
         ++launches;

@@ -164,7 +164,16 @@ struct bfs_graph_s {
     bfsb::DevBuf<int64_t> cnt_mat;   // [p*p] claim counts, row = sender
     int64_t* h_cnt_mat = nullptr;    // pinned mirror
 
-    bfs_policy policy{0, 15, 18, 0, 0};
+    // device-driven level loop (one GPU): state, per-step records, scan tile states,
+    // the instantiated loop graph and pinned mirrors for the one read-back per search
+    bfsb::DevBuf<int64_t> ctl, lrec, tstate;
+    bfsb::DevBuf<uint32_t> tctr;
+    cudaGraph_t loop_graph = nullptr;
+    cudaGraphExec_t loop_exec = nullptr;
+    int64_t* h_ctl = nullptr;
+    int64_t* h_lrec = nullptr;
+
+    bfs_policy policy{0, 15, 18, 0, 0, 0};
     std::vector<bfs_level_stats> levels;
     bfs_run_stats run{};
     int64_t last_root_l = 0;
@@ -185,6 +194,7 @@ void validate_kron_spec(const bfs_kron_spec* spec);
 // bfs.cu
 void bfs_alloc_state(bfs_graph_s* g);
 void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out);
+void bfs_release_loop(bfs_graph_s* g);
 int64_t component_tuples_impl(bfs_graph_s* g);
 void sample_roots_impl(bfs_graph_s* g, uint32_t scale, uint64_t seed, int64_t count, int64_t* roots, int64_t* found);
 // host-side Philox (product's own; used for root candidates)
