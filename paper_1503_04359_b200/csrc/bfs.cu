@@ -356,6 +356,16 @@ static int bu_long_setting() {
     return e ? std::max(1, atoi(e)) : kBuLongDefault;
 }
 
+// L2 bulk prefetch of the next batch's records (BFS_BU_PREFETCH: tuning only)
+static int bu_prefetch_setting() {
+    const char* e = getenv("BFS_BU_PREFETCH");
+    return e ? atoi(e) : 1;
+}
+
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Bottom-up step (Alg. 1 BU branch, `break for` P:107, R1).
 // A warp takes a batch of 32 visited words (1024 owned vertices) at a time from a
 // global work counter:
@@ -384,7 +394,8 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
            const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
            const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
            int32_t next_level,
-           unsigned long long* __restrict__ cnt, int grab, int blong, const Ctl* ctl, LevelRec* lrec) {
+           unsigned long long* __restrict__ cnt, int grab, int blong, int prefetch, const Ctl* ctl,
+           LevelRec* lrec) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
     __shared__ int64_t s_lj[kBuWarps][kLongCap];
@@ -423,6 +434,13 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
         const int64_t w = bt * 32 + lane;
         const uint32_t vis = w < words ? visited[w] : kFull;
         const uint32_t un = ~vis;
+        // TMA bulk prefetch of the next batch's head records (and parent labels) into
+        // L2 while this batch is probed: its loads then wait on L2, not on HBM
+        if (prefetch && lane == 0 && bt + 1 < bt_end && (bt + 1) * 1024 < words * 32) {
+            const int64_t nv = min((long long)1024, (long long)(words * 32 - (bt + 1) * 1024));
+            bulk_prefetch_l2(head + (bt + 1) * 1024, (uint32_t)(nv * 8 + 15) & ~15u);
+            if (hpar) bulk_prefetch_l2(hpar + (bt + 1) * 1024, (uint32_t)(nv * 4 + 15) & ~15u);
+        }
         if (!__ballot_sync(kFull, un != 0u)) {
             if (w < words) next[wbase + w] = 0u;
             continue;
@@ -1239,7 +1257,7 @@ static void build_loop_graph(bfs_graph_s* g) {
     const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
     add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
                g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
-               cnt, grab, bu_long_setting(), ctl, lrec);
+               cnt, grab, bu_long_setting(), bu_prefetch_setting(), ctl, lrec);
     BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
     g->loop_graph = G;
 }
@@ -1549,7 +1567,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
                                                          pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
-                                                         d + 1, cnt, grab, bu_long_setting(), nullptr,
+                                                         d + 1, cnt, grab, bu_long_setting(), bu_prefetch_setting(), nullptr,
                                                          nullptr);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
