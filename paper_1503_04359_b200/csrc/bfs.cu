@@ -40,8 +40,9 @@ namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kTdThreads = 256;
-constexpr int kTdItems = 4;
+constexpr int kTdItems = 8;
 constexpr int kTdChunk = kTdThreads * kTdItems;  // arcs per CTA iteration
+constexpr int kTdStage = 256;  // frontier entries of a chunk staged in shared memory (more: global search)
 
 // counter slots: [0, 8) written by this rank's kernels, [8, 16) global (allreduced)
 enum { C_NEXT = 0, C_MF = 1, C_INSP = 2, C_B2Q = 3, C_SCAN = 4, C_WORK = 5, C_TUPLES = 6, C_COORD = 7,
@@ -161,15 +162,15 @@ struct Remote {          // p > 1 only
 //   C  winners write depth/parent and stage v in shared memory; one atomicAdd per
 //      CTA chunk on the global queue tail, then a coalesced copy of the stage.
 template <bool kMulti>
-__global__ void __launch_bounds__(kTdThreads)
+__global__ void __launch_bounds__(kTdThreads, 5)
 k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
             const Queue qnext_in, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
             int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec) {
-    __shared__ int64_t s_pre[kTdChunk + 2];
-    __shared__ int64_t s_beg[kTdChunk + 1];
-    __shared__ int32_t s_u[kTdChunk + 1];
+    __shared__ int64_t s_pre[kTdStage + 2];
+    __shared__ int64_t s_beg[kTdStage + 1];
+    __shared__ int32_t s_u[kTdStage + 1];
     __shared__ int32_t s_q[kTdChunk];
     __shared__ int32_t s_qd[kTdChunk];
     __shared__ int s_qn;
@@ -193,7 +194,7 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         const int64_t i0 = starts[c];
         const int64_t i1 = (c + 1 < nchunks) ? starts[c + 1] : F - 1;
         const int64_t cntv = min(i1 - i0 + 1, F - i0);
-        const bool fits = cntv <= kTdChunk;
+        const bool fits = cntv <= kTdStage;
         if (fits) {
             for (int k = threadIdx.x; k <= cntv; k += kTdThreads) {
                 s_pre[k] = prefix[i0 + k];
