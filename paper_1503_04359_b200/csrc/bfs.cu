@@ -360,7 +360,7 @@ static int bu_long_setting() {
 // L2 bulk prefetch of the next batch's records (BFS_BU_PREFETCH: tuning only)
 static int bu_prefetch_setting() {
     const char* e = getenv("BFS_BU_PREFETCH");
-    return e ? atoi(e) : 1;
+    return e ? atoi(e) : 0;   // off: measured harmful (prefetches skipped batches too)
 }
 
 __device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
@@ -1279,7 +1279,19 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
                           int32_t* depth_out) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
-    if (!g->loop_exec) build_loop_graph(g);
+    // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
+    const std::vector<int> key{bu_long_setting(), bu_prefetch_setting()};
+    if (g->loop_exec && g->loop_key != key) {
+        BFS_CUDA(cudaStreamSynchronize(s));
+        cudaGraphExecDestroy(g->loop_exec);
+        cudaGraphDestroy(g->loop_graph);
+        g->loop_exec = nullptr;
+        g->loop_graph = nullptr;
+    }
+    if (!g->loop_exec) {
+        build_loop_graph(g);
+        g->loop_key = key;
+    }
     Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
     const Queue qa{g->q0.p, g->qd0.p};
     const int64_t pw = padded_words(nl);

@@ -170,6 +170,7 @@ struct bfs_graph_s {
     bfsb::DevBuf<uint32_t> tctr;
     cudaGraph_t loop_graph = nullptr;
     cudaGraphExec_t loop_exec = nullptr;
+    std::vector<int> loop_key;       // tuning knobs the graph was built with
     int64_t* h_ctl = nullptr;
     int64_t* h_lrec = nullptr;
 
