@@ -357,14 +357,11 @@ static int bu_long_setting() {
     return e ? std::max(1, atoi(e)) : kBuLongDefault;
 }
 
-// L2 bulk prefetch of the next batch's records (BFS_BU_PREFETCH: tuning only)
-static int bu_prefetch_setting() {
-    const char* e = getenv("BFS_BU_PREFETCH");
-    return e ? atoi(e) : 0;   // off: measured harmful (prefetches skipped batches too)
-}
-
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// unvisited vertices of a 1024-vertex batch from which it is probed densely
+// (BFS_BU_DENSE: tuning only)
+static int bu_dense_setting() {
+    const char* e = getenv("BFS_BU_DENSE");
+    return e ? atoi(e) : 384;
 }
 
 // Bottom-up step (Alg. 1 BU branch, `break for` P:107, R1).
@@ -395,7 +392,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
            const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
            const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
            int32_t next_level,
-           unsigned long long* __restrict__ cnt, int grab, int blong, int prefetch, const Ctl* ctl,
+           unsigned long long* __restrict__ cnt, int grab, int blong, int dense_u, const Ctl* ctl,
            LevelRec* lrec) {
     __shared__ uint16_t s_list[kBuWarps][1024];
     __shared__ uint32_t s_nb[kBuWarps][32];
@@ -435,78 +432,111 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
         const int64_t w = bt * 32 + lane;
         const uint32_t vis = w < words ? visited[w] : kFull;
         const uint32_t un = ~vis;
-        // TMA bulk prefetch of the next batch's head records (and parent labels) into
-        // L2 while this batch is probed: its loads then wait on L2, not on HBM
-        if (prefetch && lane == 0 && bt + 1 < bt_end && (bt + 1) * 1024 < words * 32) {
-            const int64_t nv = min((long long)1024, (long long)(words * 32 - (bt + 1) * 1024));
-            bulk_prefetch_l2(head + (bt + 1) * 1024, (uint32_t)(nv * 8 + 15) & ~15u);
-            if (hpar) bulk_prefetch_l2(hpar + (bt + 1) * 1024, (uint32_t)(nv * 4 + 15) & ~15u);
-        }
         if (!__ballot_sync(kFull, un != 0u)) {
             if (w < words) next[wbase + w] = 0u;
             continue;
         }
-        // 2. compact unvisited local indices (0..1023) into the per-warp list
         const int c = __popc(un);
-        int inc = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int y = __shfl_up_sync(kFull, inc, d);
-            if (lane >= d) inc += y;
-        }
-        const int U = __shfl_sync(kFull, inc, 31);
-        {
-            uint32_t bits = un;
-            int p = inc - c;
-            while (bits) {
-                const int k = __ffs(bits) - 1;
-                bits &= bits - 1;
-                list[p++] = (uint16_t)(lane * 32 + k);
-            }
-        }
+        const int U = __reduce_add_sync(kFull, c);
         nbw[lane] = 0u;
         if (lane == 0) s_lcount[wid] = 0;
         my_scan += (unsigned long long)c;
-        __syncwarp();
         const int64_t vbase = bt * 1024;
-        // 3a. first probes: every unvisited vertex tries the first neighbour of its
-        //     row from the dense head record (8 bytes, coalesced along the list);
-        //     kBuIlp records per lane are loaded before any is probed.  With rows in
-        //     canonical order this resolves most vertices.  Vertices that miss
-        //     and have more neighbours are compacted in place at the front of the list.
-        int M = 0;  // warp-uniform miss count
-        for (int t0 = 0; t0 < U; t0 += 32 * kBuIlp) {
-            int32_t sv[kBuIlp];
-            int2 hd[kBuIlp];
+        int M = 0;  // warp-uniform count of rows that missed their first probe
+        if (U >= dense_u) {
+            // 3a'. dense batch (most vertices unvisited, the first bottom-up levels):
+            //     lane j takes vertex j of every word, so head records load coalesced
+            //     and the next word of the batch is one ballot -- no list to build and
+            //     no shared-memory atomics.  Misses go to the list for 3b.
+            uint32_t mynext = 0u;
+            for (int k0 = 0; k0 < 32; k0 += kBuIlp) {
+                int32_t sv[kBuIlp];
 #pragma unroll
-            for (int k = 0; k < kBuIlp; ++k) {
-                const int idx = t0 + k * 32 + lane;
-                sv[k] = idx < U ? (int32_t)list[idx] : -1;
-            }
-#pragma unroll
-            for (int k = 0; k < kBuIlp; ++k) hd[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]) : make_int2(-1, 0);
-            // reindexed graphs: the first neighbour's ORIGINAL label comes from a dense
-            // per-vertex array read beside the head record (coalesced), not from a
-            // random ilabel[] lookup after the probe
-            int32_t po[kBuIlp];
-#pragma unroll
-            for (int k = 0; k < kBuIlp; ++k) po[k] = (hpar && sv[k] >= 0) ? __ldg(hpar + vbase + sv[k]) : hd[k].x;
-            bool hit[kBuIlp];
-#pragma unroll
-            for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front(front, hd[k].x);
-            __syncwarp();  // all lanes hold their entries of this block before misses overwrite it
-#pragma unroll
-            for (int k = 0; k < kBuIlp; ++k) {
-                if (hd[k].y > 0) my_insp += 1;
-                if (hit[k]) {
-                    __stcs(out + vbase + sv[k], make_int2(next_level, po[k]));
-                    atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
-                    my_mf += (unsigned long long)hd[k].y;
+                for (int j = 0; j < kBuIlp; ++j) {
+                    const uint32_t vk = __shfl_sync(kFull, vis, k0 + j);
+                    sv[j] = ((vk >> lane) & 1u) ? -1 : (k0 + j) * 32 + lane;
                 }
-                const bool miss = !hit[k] && hd[k].y > 1;
-                const unsigned mm = __ballot_sync(kFull, miss);
-                if (miss) list[M + __popc(mm & lanemask_lt())] = (uint16_t)sv[k];
-                M += __popc(mm);
+                int2 hd[kBuIlp];
+#pragma unroll
+                for (int j = 0; j < kBuIlp; ++j) hd[j] = sv[j] >= 0 ? __ldg(head + vbase + sv[j]) : make_int2(-1, 0);
+                int32_t po[kBuIlp];
+#pragma unroll
+                for (int j = 0; j < kBuIlp; ++j) po[j] = (hpar && sv[j] >= 0) ? __ldg(hpar + vbase + sv[j]) : hd[j].x;
+                bool hit[kBuIlp];
+#pragma unroll
+                for (int j = 0; j < kBuIlp; ++j) hit[j] = hd[j].y > 0 && in_front(front, hd[j].x);
+#pragma unroll
+                for (int j = 0; j < kBuIlp; ++j) {
+                    if (hd[j].y > 0) my_insp += 1;
+                    if (hit[j]) {
+                        __stcs(out + vbase + sv[j], make_int2(next_level, po[j]));
+                        my_mf += (unsigned long long)hd[j].y;
+                    }
+                    const unsigned hm = __ballot_sync(kFull, hit[j]);
+                    if (lane == k0 + j) mynext = hm;
+                    const bool miss = !hit[j] && hd[j].y > 1;
+                    const unsigned mm = __ballot_sync(kFull, miss);
+                    if (miss) list[M + __popc(mm & lanemask_lt())] = (uint16_t)sv[j];
+                    M += __popc(mm);
+                }
+            }
+            nbw[lane] = mynext;
+        } else {
+            // 2. compact unvisited local indices (0..1023) into the per-warp list
+            int inc = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int y = __shfl_up_sync(kFull, inc, d);
+                if (lane >= d) inc += y;
+            }
+            {
+                uint32_t bits = un;
+                int p = inc - c;
+                while (bits) {
+                    const int k = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    list[p++] = (uint16_t)(lane * 32 + k);
+                }
+            }
+            __syncwarp();
+            // 3a. first probes: every unvisited vertex tries the first neighbour of its
+            //     row from the dense head record (8 bytes, coalesced along the list);
+            //     kBuIlp records per lane are loaded before any is probed.  With rows in
+            //     canonical order this resolves most vertices.  Vertices that miss
+            //     and have more neighbours are compacted in place at the front of the list.
+            for (int t0 = 0; t0 < U; t0 += 32 * kBuIlp) {
+                int32_t sv[kBuIlp];
+                int2 hd[kBuIlp];
+#pragma unroll
+                for (int k = 0; k < kBuIlp; ++k) {
+                    const int idx = t0 + k * 32 + lane;
+                    sv[k] = idx < U ? (int32_t)list[idx] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < kBuIlp; ++k) hd[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]) : make_int2(-1, 0);
+                // reindexed graphs: the first neighbour's ORIGINAL label comes from a dense
+                // per-vertex array read beside the head record (coalesced), not from a
+                // random ilabel[] lookup after the probe
+                int32_t po[kBuIlp];
+#pragma unroll
+                for (int k = 0; k < kBuIlp; ++k) po[k] = (hpar && sv[k] >= 0) ? __ldg(hpar + vbase + sv[k]) : hd[k].x;
+                bool hit[kBuIlp];
+#pragma unroll
+                for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front(front, hd[k].x);
+                __syncwarp();  // all lanes hold their entries of this block before misses overwrite it
+#pragma unroll
+                for (int k = 0; k < kBuIlp; ++k) {
+                    if (hd[k].y > 0) my_insp += 1;
+                    if (hit[k]) {
+                        __stcs(out + vbase + sv[k], make_int2(next_level, po[k]));
+                        atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
+                        my_mf += (unsigned long long)hd[k].y;
+                    }
+                    const bool miss = !hit[k] && hd[k].y > 1;
+                    const unsigned mm = __ballot_sync(kFull, miss);
+                    if (miss) list[M + __popc(mm & lanemask_lt())] = (uint16_t)sv[k];
+                    M += __popc(mm);
+                }
             }
         }
         __syncwarp();
@@ -1258,7 +1288,7 @@ static void build_loop_graph(bfs_graph_s* g) {
     const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
     add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
                g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
-               cnt, grab, bu_long_setting(), bu_prefetch_setting(), ctl, lrec);
+               cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
     BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
     g->loop_graph = G;
 }
@@ -1280,7 +1310,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
     // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
-    const std::vector<int> key{bu_long_setting(), bu_prefetch_setting()};
+    const std::vector<int> key{bu_long_setting(), bu_dense_setting()};
     if (g->loop_exec && g->loop_key != key) {
         BFS_CUDA(cudaStreamSynchronize(s));
         cudaGraphExecDestroy(g->loop_exec);
@@ -1580,7 +1610,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
                                                          pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
-                                                         d + 1, cnt, grab, bu_long_setting(), bu_prefetch_setting(), nullptr,
+                                                         d + 1, cnt, grab, bu_long_setting(), bu_dense_setting(), nullptr,
                                                          nullptr);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
