@@ -382,7 +382,7 @@ static int bu_dense_setting() {
 //   5. the 32 next words are assembled in shared memory and stored coalesced.
 constexpr int kBuWarps = 8;
 constexpr int kBuSlots = 3;
-constexpr int kBuIlp = 4;
+constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (one aligned vector load) and probes per round
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
