@@ -1017,12 +1017,14 @@ __global__ void k_td_prep(const Ctl* ctl, const uint32_t* __restrict__ f0, const
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue qa, Queue qb, int64_t* __restrict__ out,
-                                                           unsigned long long* tstate, unsigned int* tctr) {
+__global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue qa, Queue qb, int64_t n_host,
+                                                           int64_t* __restrict__ out, unsigned long long* tstate,
+                                                           unsigned int* tctr) {
     __shared__ long long s_tile, s_excl;
     __shared__ long long s_warp[kScanThreads / 32];
-    const long long n = ctl->n_f;
-    const int32_t* __restrict__ deg = ctl->qsel ? qb.deg : qa.deg;
+    // loop graph: size and queue from the loop state; host loop: qa holds the queue
+    const long long n = ctl ? ctl->n_f : n_host;
+    const int32_t* __restrict__ deg = (ctl && ctl->qsel) ? qb.deg : qa.deg;
     const long long tiles = (n + kScanTile - 1) / kScanTile;
     if (n == 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
@@ -1113,6 +1115,8 @@ void bfs_alloc_state(bfs_graph_s* g) {
     const int64_t nl = g->nl();
     const int p = g->comm ? g->comm->nranks : 1;
     g->visited.alloc((size_t)padded_words(nl), s);
+    g->tstate.alloc((size_t)(nl / kScanTile + 2), s);   // single-pass scan tile states
+    g->tctr.alloc(1, s);
     // global bitmaps: p slices of nb/32 words (nb is a multiple of 32)
     const int64_t gwords = p > 1 ? (int64_t)p * (g->nb / 32) : padded_words(g->n);
     g->front.alloc((size_t)gwords + 4, s);
@@ -1244,8 +1248,6 @@ static void build_loop_graph(bfs_graph_s* g) {
     if (!g->ctl.p) {
         g->ctl.alloc(sizeof(Ctl) / 8, s);
         g->lrec.alloc((size_t)kGraphMaxLevels * sizeof(LevelRec) / 8, s);
-        g->tstate.alloc((size_t)(nl / kScanTile + 2), s);
-        g->tctr.alloc(1, s);
         BFS_CUDA(cudaMallocHost(&g->h_ctl, sizeof(Ctl) + kLrecHead * sizeof(LevelRec)));
         BFS_CUDA(cudaMallocHost(&g->h_lrec, (size_t)kGraphMaxLevels * sizeof(LevelRec)));
     }
@@ -1273,8 +1275,8 @@ static void build_loop_graph(bfs_graph_s* g) {
     // top-down body
     cudaGraphNode_t t1 = add_kernel(T, {}, k_td_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words, g->head.p, qa, qb,
                                     cnt, tstate, g->tctr.p);
-    cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, g->prefix.p, tstate,
-                                    g->tctr.p);
+    cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, (int64_t)0, g->prefix.p,
+                                    tstate, g->tctr.p);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
                                     g->scratch64.p, ctl);
     add_kernel(T, {t3}, k_td_expand<false>, g8, dim3(kTdThreads), 0, qa, g->prefix.p, g->scratch64.p, (int64_t)0,
@@ -1538,7 +1540,14 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             if (E > 0) {
                 l2_window(g, g->visited.p, g->visited.bytes());
-                launches += scan_exclusive_i32(qcur.deg, g->prefix.p, nf_loc, s);
+                // single-pass scan of the queue degrees (the loop graph's kernel, host-sized)
+                BFS_CUDA(cudaMemsetAsync(g->tstate.p, 0, (size_t)((nf_loc + kScanTile - 1) / kScanTile) * 8, s));
+                BFS_CUDA(cudaMemsetAsync(g->tctr.p, 0, sizeof(uint32_t), s));
+                k_scan_dev<<<grid_for((nf_loc + kScanTile - 1) / kScanTile * kScanThreads, kScanThreads), kScanThreads, 0,
+                             s>>>(nullptr, qcur, qcur, nf_loc, g->prefix.p, (unsigned long long*)g->tstate.p,
+                                  g->tctr.p);
+                BFS_CHECK_LAUNCH();
+                ++launches;
                 const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
                 k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p,
                                                                           nullptr);

@@ -84,10 +84,6 @@ int num_sms();
 // Input is int32 or int64 array; out may alias in only when both are int64.
 int scan_exclusive_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
 int scan_exclusive_i32(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);
-// out[i] for i in [0, F]: prefix of row lengths of queue entries q[i] (degree of q[i]),
-// len(q[i]) = off[q[i]-lo+1] - off[q[i]-lo]
-int scan_queue_degrees(const int32_t* q, int64_t F, const int64_t* off, int64_t lo, int64_t* out,
-                        cudaStream_t s);
 
 }  // namespace bfsb
 

@@ -23,15 +23,6 @@ struct LoadI32 {
     const int32_t* p;
     __device__ int64_t operator()(int64_t i) const { return p[i]; }
 };
-struct LoadQueueDeg {
-    const int32_t* q;
-    const int64_t* off;
-    int64_t lo;
-    __device__ int64_t operator()(int64_t i) const {
-        int64_t v = (int64_t)q[i] - lo;
-        return off[v + 1] - off[v];
-    }
-};
 
 __device__ __forceinline__ int64_t warp_incl_scan(int64_t x) {
     const int lane = threadIdx.x & 31;
@@ -149,9 +140,5 @@ int scan_exclusive_i32(const int32_t* in, int64_t* out, int64_t n, cudaStream_t 
     return scan_impl(LoadI32{in}, n, out, s);
 }
 
-int scan_queue_degrees(const int32_t* q, int64_t F, const int64_t* off, int64_t lo, int64_t* out,
-                        cudaStream_t s) {
-    return scan_impl(LoadQueueDeg{q, off, lo}, F, out, s);
-}
 
 }  // namespace bfsb
