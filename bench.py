@@ -213,6 +213,11 @@ def main():
     # (profiles/r01_switch_sweep.txt); the parity tests cover 15/18 and other settings
     ap.add_argument("--alpha", type=int, default=30)
     ap.add_argument("--beta", type=int, default=24)
+    ap.add_argument("--policy", default="do", choices=["do", "td", "paper"],
+                    help="do: Beamer alpha/beta (default); td: top-down only (classic, P:202); "
+                         "paper: the paper's section 3.3 rule (policy mode 3, --paper-alpha/--paper-beta)")
+    ap.add_argument("--paper-alpha", type=int, default=500, help="static fraction of arcs, 1/10000 units (S:320)")
+    ap.add_argument("--paper-beta", type=int, default=3, help="bottom-up steps before returning top-down (S:321)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--reindex", type=int, default=1, help="section 3.4 degree reindex (P:158)")
     ap.add_argument("--rows", default="id", choices=["id", "degree"],
@@ -259,7 +264,12 @@ def main():
     nl = g.local_end - g.local_begin
     parent = torch.empty(nl, dtype=torch.int32, device="cuda")
     depth = torch.empty(nl, dtype=torch.int32, device="cuda")
-    g.set_policy(mode=0, alpha=args.alpha, beta=args.beta, level_times=True)
+    if args.policy == "td":
+        g.set_policy(mode=1, level_times=True)
+    elif args.policy == "paper":
+        g.set_policy(mode=3, alpha=args.paper_alpha, beta=args.paper_beta, level_times=True)
+    else:
+        g.set_policy(mode=0, alpha=args.alpha, beta=args.beta, level_times=True)
 
     def one(r):
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -356,7 +366,9 @@ def main():
         "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": {"workload": cfg["name"], "scale": cfg["scale"], "edgefactor": cfg["ef"], "seed": cfg["seed"],
-                   "roots": len(roots), "alpha": args.alpha, "beta": args.beta, "parallelism": f"1d{ws}",
+                   "roots": len(roots), "policy": args.policy,
+                   "alpha": args.paper_alpha if args.policy == "paper" else args.alpha,
+                   "beta": args.paper_beta if args.policy == "paper" else args.beta, "parallelism": f"1d{ws}",
                    "reindex_by_degree": bool(args.reindex), "row_order": args.rows,
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((8 * (n + 1) + 4 * g.arcs) / 1e9)},
         "build_ms": round(build_ms, 2), "arcs": g.arcs,

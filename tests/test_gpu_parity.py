@@ -275,3 +275,18 @@ def test_graph_and_host_loops_agree_kronecker():
         assert out[0][2]["reached"] == out[1][2]["reached"]
         assert out[0][2]["component_edge_tuples"] == out[1][2]["component_edge_tuples"]
     g.close()
+
+
+def test_edge_list_file_ingestion(tmp_path):
+    """f4: an edge list read from a text file builds the same graph as the oracle's."""
+    from paper_1503_04359_b200.edgelist import load_edge_list
+    n0, e = graphs.skewed_edges(3000, 20000, 9)
+    e = np.asarray(e).reshape(-1, 2) * 7 + 11          # sparse file IDs, relabeled densely
+    p = tmp_path / "g.txt"
+    p.write_text("# skewed test graph\n" + "".join(f"{u} {v}\n" for u, v in e))
+    uv, n, ids = load_edge_list(str(p))
+    ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    g = pkg.Graph.from_edges(uv, n)
+    for root in (0, int(np.argmax(ref.degree()))):
+        _check_run(g, ref, root, dict(mode=0), uv)
+    g.close()
