@@ -209,10 +209,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(CONFIGS))
     ap.add_argument("--roots", type=int, default=ROOTS)
-    # alpha/beta: the paper gives no values (R2); 30/24 is the B200 sweep optimum
+    # alpha/beta: the paper gives no values (R2); 30/1000 is the B200 sweep optimum
     # (profiles/r01_switch_sweep.txt); the parity tests cover 15/18 and other settings
     ap.add_argument("--alpha", type=int, default=30)
-    ap.add_argument("--beta", type=int, default=24)
+    ap.add_argument("--beta", type=int, default=1000)
     ap.add_argument("--policy", default="do", choices=["do", "td", "paper"],
                     help="do: Beamer alpha/beta (default); td: top-down only (classic, P:202); "
                          "paper: the paper's section 3.3 rule (policy mode 3, --paper-alpha/--paper-beta)")

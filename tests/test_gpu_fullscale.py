@@ -57,7 +57,7 @@ def test_fullscale_properties(name):
     edges = np.concatenate(samples)   # 512K oracle edges for the V4 check
 
     g = pkg.Graph.kronecker(scale, ef, seed, abc, opts=pkg.default_opts(reindex_by_degree=True))
-    g.set_policy(mode=0, alpha=30, beta=24)
+    g.set_policy(mode=0, alpha=30, beta=1000)
     lab = torch.empty(n, dtype=torch.int32, device="cuda")
     pkg.bfs_graph_export_labels(g.h, lab)
     label = lab.cpu().numpy()

@@ -24,7 +24,7 @@ cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)
 g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], opts=pkg.default_opts(reindex_by_degree=True))
 roots = g.sample_roots(cfg["scale"], cfg["seed"], a.roots)
-pols = {"TD-only": dict(mode=1), "DO a30/b24": dict(mode=0, alpha=30, beta=24),
+pols = {"TD-only": dict(mode=1), "DO a30/b1000": dict(mode=0, alpha=30, beta=1000),
         "paper 0.05/3": dict(mode=3, alpha=500, beta=3)}
 print(f"# {cfg['name']}, per-level device ms (direction T/B, frontier size), total ms and GTEPS per search")
 for r in roots:

@@ -21,7 +21,7 @@ ap.add_argument("--skip", type=int, default=0, help="roots to skip (sampled orde
 ap.add_argument("--mode", type=int, default=0)
 ap.add_argument("--reindex", type=int, default=0)
 ap.add_argument("--alpha", type=int, default=30)
-ap.add_argument("--beta", type=int, default=24)
+ap.add_argument("--beta", type=int, default=1000)
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)

@@ -23,7 +23,7 @@ ap.add_argument("--var", required=True)
 ap.add_argument("--values", required=True)
 ap.add_argument("--roots", type=int, default=64)
 ap.add_argument("--alpha", type=int, default=30)
-ap.add_argument("--beta", type=int, default=24)
+ap.add_argument("--beta", type=int, default=1000)
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)
