@@ -1599,18 +1599,66 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             scanned = nf_loc;
         } else {
             // ---------------- bottom-up (Alg. 1, pull Alg. 3)
-            if (have_queue) {
-                BFS_CUDA(cudaMemsetAsync(front + (g->lo >> 5), 0, (size_t)words_of(nl) * 4, s));
+            // Pull (Alg. 3) adapts to the frontier's density: a sparse global
+            // frontier (4 bytes per vertex below the bitmap slices' size) travels as
+            // vertex lists -- each rank sends its owned frontier vertices to every peer and
+            // rebuilds the whole bitmap locally -- a dense one as bitmap slices (allgather).
+            // Every rank sees the same global n_f, so all take the same branch.
+            const bool sparse_pull = mg && (uint64_t)n_f * 4 < (uint64_t)slice_bytes * (uint64_t)(p - 1);
+            if (sparse_pull) {
+                // this rank's frontier as a vertex list: the TD queue, or its bitmap slice
+                const int32_t* mine = qcur.v;
+                if (!have_queue) {
+                    k_b2q<<<grid_for(words, 256), 256, 0, s>>>(front, words, g->lo, g->head.p, qnxt, cnt);
+                    BFS_CHECK_LAUNCH();
+                    ++launches;
+                    mine = qnxt.v;
+                }
+                BFS_CUDA(cudaMemsetAsync(g->cnt_mat.p, 0, (size_t)p * 8, s));
+                BFS_CUDA(cudaMemcpyAsync(g->cnt_mat.p + me, &g->h_cnt[C_NEXT], 8, cudaMemcpyHostToDevice, s));
+                g->comm->allgather_inplace(g->cnt_mat.p, 8, s);
+                BFS_CUDA(cudaMemcpyAsync(g->h_cnt_mat, g->cnt_mat.p, (size_t)p * 8, cudaMemcpyDeviceToHost, s));
+                BFS_CUDA(cudaStreamSynchronize(s));
+                int64_t R = 0;
+                for (int q = 0; q < p; ++q) R += q == me ? 0 : g->h_cnt_mat[q];
+                ensure(g->flist, (size_t)std::max<int64_t>(R, 1), s);
+                int64_t roff = 0;
+                for (int q = 0; q < p; ++q) {
+                    const int64_t in_q = q == me ? 0 : g->h_cnt_mat[q];
+                    sendp[q] = mine;
+                    sendb[q] = q == me ? 0 : (size_t)nf_loc * 4;
+                    recvp[q] = g->flist.p + roff;
+                    recvb[q] = (size_t)in_q * 4;
+                    roff += in_q;
+                    nvl += sendb[q];
+                }
+                g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
+                BFS_CUDA(cudaMemsetAsync(front, 0, (size_t)p * slice_bytes, s));
                 if (nf_loc) {
-                    k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur.v, nf_loc, front);
+                    k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(mine, nf_loc, front);
+                    BFS_CHECK_LAUNCH();
+                    ++launches;
+                }
+                if (R) {
+                    k_q2b<<<grid_for(R, 256), 256, 0, s>>>(g->flist.p, R, front);
                     BFS_CHECK_LAUNCH();
                     ++launches;
                 }
                 have_queue = false;
-            }
-            if (mg) {
-                g->comm->allgather_inplace(front, slice_bytes, s);
-                nvl = slice_bytes * (size_t)(p - 1);
+            } else {
+                if (have_queue) {
+                    BFS_CUDA(cudaMemsetAsync(front + (g->lo >> 5), 0, (size_t)words_of(nl) * 4, s));
+                    if (nf_loc) {
+                        k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur.v, nf_loc, front);
+                        BFS_CHECK_LAUNCH();
+                        ++launches;
+                    }
+                    have_queue = false;
+                }
+                if (mg) {
+                    g->comm->allgather_inplace(front, slice_bytes, s);
+                    nvl = slice_bytes * (size_t)(p - 1);
+                }
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             l2_window(g, front, g->front.bytes());

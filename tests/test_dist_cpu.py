@@ -53,6 +53,7 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
     n_f, m_f, m_fc = allreduce([len(queue), int(sum(deg[v] for v in queue)), coord(queue)])
     direction, prev, seen_deg, steps = 0, 0, 0, []
     bu_done, returned = 0, False
+    sparse_pulls = [0]
     front = np.zeros(p * nb, bool)
     d = 0
     while n_f > 0:
@@ -106,13 +107,35 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
                         visited[v - lo] = True
                         depth[v - lo] = d + 1
                         nxt.append(v)
-        else:
-            mine = np.zeros(nb, bool)
-            for v in queue:
-                mine[v - lo] = True
-            parts = [torch.zeros(nb, dtype=torch.bool) for _ in range(p)]
-            dist.all_gather(parts, torch.from_numpy(mine))      # pull: overwrite every view
-            front = torch.cat(parts).numpy()
+        elif 4 * n_f < (nb // 8) * (p - 1):
+            # sparse pull: owned frontier vertices as lists, bitmap rebuilt locally
+            counts = [torch.zeros(1, dtype=torch.int64) for _ in range(p)]
+            dist.all_gather(counts, torch.tensor([len(queue)], dtype=torch.int64))
+            recv = [torch.zeros(int(counts[q].item()), dtype=torch.int64) for q in range(p)]
+            reqs = []
+            for q in range(p):
+                if q == rank:
+                    continue
+                if len(queue):
+                    reqs.append(dist.isend(torch.tensor(queue, dtype=torch.int64), q))
+                if recv[q].numel():
+                    reqs.append(dist.irecv(recv[q], q))
+            for r in reqs:
+                r.wait()
+            front = np.zeros(p * nb, bool)
+            front[np.asarray(queue, np.int64)] = True
+            for q in range(p):
+                if q != rank:
+                    front[recv[q].numpy()] = True
+            sparse_pulls[0] += 1
+        if direction == 1:
+            if not (4 * n_f < (nb // 8) * (p - 1)):
+                mine = np.zeros(nb, bool)
+                for v in queue:
+                    mine[v - lo] = True
+                parts = [torch.zeros(nb, dtype=torch.bool) for _ in range(p)]
+                dist.all_gather(parts, torch.from_numpy(mine))      # pull: overwrite every view
+                front = torch.cat(parts).numpy()
             for vl in np.nonzero(~visited)[0]:
                 for u in ref.row(lo + vl):
                     insp += 1
@@ -127,7 +150,7 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
         prev, n_f, m_f, m_fc = n_f, got[0], got[1], got[3]
         queue = nxt
         d += 1
-    return depth, steps
+    return depth, steps, sparse_pulls[0]
 
 
 def _worker(rank, world, port, q):
@@ -144,7 +167,7 @@ def _worker(rank, world, port, q):
             nb = pkg.bfs_partition_range(n, world, 0)[1]
             for root in sorted({0, n - 1, int(np.argmax(g.degree()))}):
                 for mode, alpha, beta in ((0, 15, 18), (1, 15, 18), (3, 500, 2), (3, 40, 3)):
-                    depth, steps = _partitioned_bfs(g, root, lo, hi, nb, world, rank, alpha, beta, mode)
+                    depth, steps, sp = _partitioned_bfs(g, root, lo, hi, nb, world, rank, alpha, beta, mode)
                     full = [None] * world
                     dist.all_gather_object(full, depth.tolist())
                     want, _ = oracle.bfs(g, root)
@@ -152,7 +175,7 @@ def _worker(rank, world, port, q):
                     ok_depth = np.array_equal(np.concatenate(full), want)
                     emu_steps = list(zip(emu["dir"].tolist(), emu["n_f"].tolist(), emu["discovered"].tolist(),
                                          emu["m_f"].tolist(), emu["m_u"].tolist(), emu["insp"].tolist()))
-                    out.append((ok_depth, steps == emu_steps))
+                    out.append((ok_depth, steps == emu_steps, sp))
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -172,5 +195,6 @@ def test_two_rank_protocol_gloo():
         pr.join(timeout=60)
     for r in (0, 1):
         assert res[r], "no cases ran"
-        for ok_depth, ok_steps in res[r]:
+        for ok_depth, ok_steps, _ in res[r]:
             assert ok_depth and ok_steps
+        assert sum(x[2] for x in res[r]) > 0, "the sparse (vertex-list) pull was never exercised"

@@ -118,10 +118,19 @@ def test_kronecker_s14(p, abc):
     assert np.array_equal(roots[0], oracle.sample_roots(ref, scale, seed, 6))
     pols = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=0, alpha=2, beta=4),
             dict(mode=3, alpha=500, beta=3), dict(mode=3, alpha=100, beta=2)]
+    slice_bytes = pkg.bfs_partition_range(ref.n, p, 0)[1] // 8
+    sparse_pulls = 0
     for i, r in enumerate(roots[0]):
         runs, levels = _check(gs, ref, r, pols[i % len(pols)], uv)
         if p > 1:
             assert sum(x["nvlink_bytes"] for x in levels[0]) == runs[0]["nvlink_bytes"]
+            # bottom-up pulls: bitmap slices when dense, vertex lists when sparse
+            for lv in levels[0]:
+                if lv["direction"] == 1 and 4 * lv["frontier"] < slice_bytes * (p - 1):
+                    sparse_pulls += 1
+                    assert lv["nvlink_bytes"] < slice_bytes * (p - 1)
+    if p > 1:
+        assert sparse_pulls > 0
     _close(comms, gs)
 
 
