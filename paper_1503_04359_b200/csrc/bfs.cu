@@ -259,6 +259,17 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         }
         // C: outputs + staged queue append; remote claims go to the owner's list
 #pragma unroll
+        // winners' degrees (8-byte head records) and parent labels: all loads issued
+        // before any is consumed, so their latencies overlap instead of adding up
+        int32_t dgs[kTdItems], par[kTdItems];
+#pragma unroll
+        for (int j = 0; j < kTdItems; ++j) {
+            // one-shot random accesses stream through L2 with evict-first so the
+            // visited words the probes and claims hit stay resident
+            dgs[j] = (win[j] && own[j]) ? __ldcs(head + (v[j] - lo)).y : 0;
+            par[j] = (win[j] && own[j] && pmap) ? __ldg(pmap + u[j]) : u[j];
+        }
+#pragma unroll
         for (int j = 0; j < kTdItems; ++j) {
             const bool lw = win[j] && own[j];
             const unsigned m = __ballot_sync(kFull, lw);
@@ -270,13 +281,10 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
                 if (lw) {
                     const int64_t vl = v[j] - lo;
                     const int slot = base + __popc(m & lanemask_lt());
-                    // one-shot random accesses stream through L2 with evict-first so the
-                    // visited words the probes and claims hit stay resident
-                    const int32_t dg = __ldcs(head + vl).y;
                     s_q[slot] = v[j];
-                    s_qd[slot] = dg;
-                    __stcs(out + vl, make_int2(next_level, pmap ? pmap[u[j]] : u[j]));
-                    my_mf += (unsigned long long)dg;
+                    s_qd[slot] = dgs[j];
+                    __stcs(out + vl, make_int2(next_level, par[j]));
+                    my_mf += (unsigned long long)dgs[j];
                 }
             }
             if (kMulti) {
@@ -1106,6 +1114,22 @@ int grid_for(int64_t items, int threads, int per_sm = 8) {
     return (int)std::max<int64_t>(1, std::min(b, cap));
 }
 
+// CTAs of the top-down kernel that are resident at once: its chunk loop is
+// grid-strided, so a grid larger than one wave would leave a straggling second wave
+template <bool kMulti>
+int td_resident_grid() {
+    static const int g = [] {
+        int per = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_td_expand<kMulti>, kTdThreads, 0) != cudaSuccess ||
+            per < 1) {
+            cudaGetLastError();
+            per = 1;
+        }
+        return per * num_sms();
+    }();
+    return g;
+}
+
 bool multi(const bfs_graph_s* g) { return g->comm && g->comm->nranks > 1; }
 
 }  // namespace
@@ -1279,7 +1303,7 @@ static void build_loop_graph(bfs_graph_s* g) {
                                     tstate, g->tctr.p);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
                                     g->scratch64.p, ctl);
-    add_kernel(T, {t3}, k_td_expand<false>, g8, dim3(kTdThreads), 0, qa, g->prefix.p, g->scratch64.p, (int64_t)0,
+    add_kernel(T, {t3}, k_td_expand<false>, dim3(td_resident_grid<false>()), dim3(kTdThreads), 0, qa, g->prefix.p, g->scratch64.p, (int64_t)0,
                (int64_t)0, g->off.p, g->adj.p, g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo,
                g->hi, Remote{}, ctl, lrec);
     // bottom-up body
@@ -1552,7 +1576,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p,
                                                                           nullptr);
                 BFS_CHECK_LAUNCH();
-                const int grid = grid_for(nchunks * kTdThreads, kTdThreads, 8);
+                const int grid = (int)std::min<int64_t>(nchunks, mg ? td_resident_grid<true>() : td_resident_grid<false>());
                 if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
                                                                   g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt, d + 1,
