@@ -41,6 +41,8 @@ CONFIGS = {
 DEFAULT_CONFIG = "k29"
 METRIC = "Graph500 harmonic-mean GTEPS (64 roots)"
 ROOTS = 64
+# random 4-byte L2 probes per second on B200 (measured: profiles/r01_l2_probe_micro.txt)
+L2_PROBE_PEAK = 270.0
 # cpu_baseline / reference arm sample: the oracle cannot build s26+ within the bench budget
 SAMPLE_SCALE = 20
 
@@ -294,6 +296,7 @@ def main():
 
     times, launches = [], 0
     kern = {"bu": [0.0, 0, 0], "td": [0.0, 0, 0]}   # ms, bytes, launches
+    probes = {"bu": 0, "td": 0}                      # frontier / visited probes (= inspections)
     levels_dump = []
     nvl_level_bytes = []
     barrier()
@@ -312,6 +315,7 @@ def main():
                     kern[key][0] += lv["kernel_ms"]
                     kern[key][1] += bu_bytes(n, lv) if key == "bu" else td_bytes(lv)
                     kern[key][2] += 1
+                    probes[key] += lv["inspections"]
                 if step == 0:
                     levels_dump.append({"root": int(r), "ms": ms, "levels": levels})
         barrier()
@@ -384,6 +388,12 @@ def main():
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
                      "share_of_step": round(share, 4), "launches": klaunch,
                      "bytes_per_launch": int(kbytes / klaunch) if klaunch else 0},
+        # second roofline for the probe-bound levels: every inspection is one random
+        # 4-byte bitmap probe; B200 serves <= ~270 G such probes/s from L2
+        # (profiles/r01_l2_probe_micro.txt, tools/micro/l2probe.cu)
+        "probe_roofline": {"bound": "l2_random_probe", "unit": "Gprobe/s", "peak": L2_PROBE_PEAK,
+                           "bu_achieved": round(probes["bu"] / (kern["bu"][0] * 1e-3) / 1e9, 2) if kern["bu"][0] else None,
+                           "td_achieved": round(probes["td"] / (kern["td"][0] * 1e-3) / 1e9, 2) if kern["td"][0] else None},
         "gpu_launches": launches,
         "nvlink": None if ws == 1 else {
             "bytes_per_level_max": max(nvl_level_bytes) if nvl_level_bytes else 0,

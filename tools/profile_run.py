@@ -19,6 +19,7 @@ ap.add_argument("--config", default="k26")
 ap.add_argument("--roots", type=int, default=2)
 ap.add_argument("--skip", type=int, default=0, help="roots to skip (sampled order)")
 ap.add_argument("--mode", type=int, default=0)
+ap.add_argument("--root", type=int, default=-1, help="run this root (original label) instead of sampled ones")
 ap.add_argument("--reindex", type=int, default=0)
 ap.add_argument("--alpha", type=int, default=30)
 ap.add_argument("--beta", type=int, default=1000)
@@ -28,7 +29,7 @@ torch.cuda.set_device(0)
 g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"],
                         opts=pkg.default_opts(reindex_by_degree=bool(a.reindex)))
 print("build_ms", g.build_ms, flush=True)
-roots = g.sample_roots(cfg["scale"], cfg["seed"], a.skip + a.roots)[a.skip:]
+roots = [a.root] if a.root >= 0 else g.sample_roots(cfg["scale"], cfg["seed"], a.skip + a.roots)[a.skip:]
 g.set_policy(mode=a.mode, alpha=a.alpha, beta=a.beta, level_times=True)
 for r in roots:
     p, d = g.run(int(r))
