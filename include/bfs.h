@@ -90,18 +90,19 @@ typedef struct {
  *           "static percent" in units of 1/10000 (500 = 0.05); after beta BU
  *           steps ("a fixed number of steps") return to TD for the rest of the search.
  * level_times != 0 records per-step device times into bfs_level_stats.ms / kernel_ms.
- * host_loop: 0 = on one GPU the level loop runs on the device as one CUDA graph
- *   (conditional WHILE/IF nodes) with one host synchronisation per search;
- *   on p ranks the host drives the levels (the exchange sizes are host decisions).
- *   1 = host-driven loop everywhere (one synchronisation per level).  Both give
- *   identical outputs and statistics.
- * Defaults: mode 0, alpha 15, beta 18, bu_from_level 0, level_times 0, host_loop 0. */
+ * loop (who drives the levels): 0 = auto: on one GPU a device-driven loop,
+ *   the persistent one-kernel search for graphs up to 2^22 arcs, the CUDA loop graph
+ *   (conditional WHILE/IF nodes) above; on p ranks the host (the exchange sizes are
+ *   host decisions).  1 = host-driven loop (one synchronisation per level).  2 = the
+ *   loop graph, 3 = the persistent kernel (one GPU; else host).  All give identical
+ *   outputs and statistics (one host synchronisation per search on the device loops).
+ * Defaults: mode 0, alpha 15, beta 18, bu_from_level 0, level_times 0, loop 0. */
 typedef struct {
     int mode;
     int64_t alpha, beta;
     int bu_from_level;
     int level_times;
-    int host_loop;
+    int loop;
 } bfs_policy;
 
 /* One record per BFS step d (the step that builds level d+1 from frontier d). */

@@ -53,7 +53,7 @@ class bfs_build_opts(ctypes.Structure):
 
 class bfs_policy(ctypes.Structure):
     _fields_ = [("mode", ctypes.c_int), ("alpha", ctypes.c_int64), ("beta", ctypes.c_int64),
-                ("bu_from_level", ctypes.c_int), ("level_times", ctypes.c_int), ("host_loop", ctypes.c_int)]
+                ("bu_from_level", ctypes.c_int), ("level_times", ctypes.c_int), ("loop", ctypes.c_int)]
 
 
 class bfs_level_stats(ctypes.Structure):
@@ -193,9 +193,14 @@ def bfs_graph_build_ms(h) -> float:
     return x.value
 
 
+LOOPS = {"auto": 0, "host": 1, "graph": 2, "persistent": 3}
+
+
 def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_level: int = 0, level_times: bool = False,
-                   host_loop: bool = False):
-    p = bfs_policy(mode, alpha, beta, bu_from_level, int(level_times), int(host_loop))
+                   loop="auto", host_loop: bool = False):
+    """loop: 'auto' | 'host' | 'graph' | 'persistent' (or 0..3); host_loop=True is loop='host'."""
+    lp = 1 if host_loop else (LOOPS[loop] if isinstance(loop, str) else int(loop))
+    p = bfs_policy(mode, alpha, beta, bu_from_level, int(level_times), lp)
     _check(lib().bfs_set_policy(h, ctypes.byref(p)))
 
 

@@ -83,7 +83,7 @@ struct Ctl {
     long long root_i;         // internal label of the root
     long long alpha, beta, n, arcs;
     int d, dir, have_queue, qsel, fsel, bu_done, returned, overflow;
-    int mode, bu_from, max_levels, pad;
+    int mode, bu_from, max_levels, done;   // done: the persistent kernel's stop flag
 };
 // one record per step, filled by the step kernels (times: %globaltimer ns)
 struct LevelRec {
@@ -935,14 +935,11 @@ __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __res
     }
 }
 
-__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_td,
-                             cudaGraphConditionalHandle h_bu) {
-    Ctl c = *ctl;
-    const long long t = gtimer();
+// the step's bookkeeping and direction (the host loop's rule, verbatim); returns m_u(d)
+__device__ __forceinline__ long long step_decide(Ctl& c) {
     c.reached += c.n_f;
     c.seen += c.m_f;
     const long long m_u = c.arcs - c.seen;
-    // direction for the step that builds level d+1: the host loop's rule, verbatim
     switch (c.mode) {
         case 1: c.dir = 0; break;
         case 2: c.dir = c.d >= c.bu_from ? 1 : 0; break;
@@ -962,6 +959,41 @@ __global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, 
                 if (c.n_f * c.beta < c.n && c.n_f < c.prev_nf) c.dir = 0;
             }
     }
+    return m_u;
+}
+
+// the step's record and the roll of the counters into the loop state (k_step_end and
+// the persistent kernel); returns whether the search continues
+__device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned long long* cnt) {
+    const long long next = (long long)cnt[C_NEXT], mf = (long long)cnt[C_MF];
+    r.discovered = next;
+    r.insp = c.dir == 0 ? c.m_f : (long long)cnt[C_INSP];
+    r.scanned = c.dir == 0 ? c.n_f : (long long)cnt[C_SCAN];
+    r.te = gtimer();
+    if (c.dir == 0) {
+        c.qsel ^= 1;
+        c.have_queue = 1;
+    } else {
+        c.fsel ^= 1;
+        c.have_queue = 0;
+    }
+    c.prev_nf = c.n_f;
+    c.n_f = next;
+    c.m_f = c.m_fc = mf;
+    c.d += 1;
+    bool cont = next > 0;
+    if (cont && c.d >= c.max_levels) {
+        c.overflow = 1;
+        cont = false;
+    }
+    return cont;
+}
+
+__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_td,
+                             cudaGraphConditionalHandle h_bu) {
+    Ctl c = *ctl;
+    const long long t = gtimer();
+    const long long m_u = step_decide(c);
     c.E = c.m_f;
     c.nchunks = (c.E + kTdChunk - 1) / kTdChunk;
     LevelRec r{};
@@ -980,30 +1012,9 @@ __global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, 
 
 __global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* cnt, cudaGraphConditionalHandle h_loop) {
     Ctl c = *ctl;
-    LevelRec& r = lrec[c.d];
-    const long long next = (long long)cnt[C_NEXT], mf = (long long)cnt[C_MF];
-    r.discovered = next;
-    r.insp = c.dir == 0 ? c.m_f : (long long)cnt[C_INSP];
-    r.scanned = c.dir == 0 ? c.n_f : (long long)cnt[C_SCAN];
-    r.te = gtimer();
-    if (c.dir == 0) {
-        c.qsel ^= 1;
-        c.have_queue = 1;
-    } else {
-        c.fsel ^= 1;
-        c.have_queue = 0;
-    }
-    c.prev_nf = c.n_f;
-    c.n_f = next;
-    c.m_f = c.m_fc = mf;
-    c.d += 1;
-    int cont = next > 0;
-    if (cont && c.d >= c.max_levels) {
-        c.overflow = 1;
-        cont = 0;
-    }
+    const bool cont = step_finish(c, lrec[c.d], cnt);
     *ctl = c;
-    cudaGraphSetConditional(h_loop, (unsigned)cont);
+    cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
 }
 
 // top-down prologue: frontier bitmap -> queue when the previous step was bottom-up,
@@ -1106,6 +1117,223 @@ __global__ void k_bu_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* _
 __global__ void k_q2b_dev(const Ctl* ctl, Queue qa, Queue qb, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1) {
     if (!ctl->have_queue) return;
     q2b_body((ctl->qsel ? qb : qa).v, ctl->n_f, ctl->fsel ? f1 : f0);
+}
+
+// ============================================================ persistent search
+// (the cooperative-kernel variant) for small graphs, where even a graph
+// node costs more than a level's work: ONE kernel, sized to one resident wave, runs every level of a
+// search, the phases separated by grid-wide barriers.  Same state (Ctl, LevelRec,
+// queues, bitmaps, records) and the same step semantics as the other loops:
+//   TD: warp per frontier vertex of degree < kPersBig, then every big row split over
+//       the whole grid; claims by atomicOr on the visited word; winners append to the
+//       next queue (warp-aggregated) and record (depth, parent)
+//   BU: warp per visited word, lane per vertex, row scanned in stored order up to the
+//       first frontier neighbour (its parent); the next word is the warp's ballot
+// Data other blocks wrote during the search is read with ld.global.cg (L1 is not
+// coherent across the grid barrier); the CSR is read-only.
+constexpr int kPersThreads = 256;
+constexpr int kPersBig = 2048;   // rows at least this long are split over the grid
+
+// Grid-wide barrier for a grid no larger than one resident wave (the launch sizes it
+// from the occupancy): arrive on a counter; the last block resets it and bumps the
+// generation the others spin on.  (cooperative_groups' grid sync needs a cooperative
+// launch, measured ~60 us more per search on B200.)
+struct GridBar {
+    unsigned* count;
+    unsigned* gen;
+    __device__ __forceinline__ void sync() const {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned g = *(volatile unsigned*)gen;
+            __threadfence();
+            if (atomicAdd(count, 1u) == gridDim.x - 1) {
+                *(volatile unsigned*)count = 0u;
+                __threadfence();
+                atomicAdd(gen, 1u);
+            } else {
+                while (*(volatile unsigned*)gen == g) __nanosleep(32);
+            }
+            __threadfence();
+        }
+        __syncthreads();
+    }
+};
+
+__device__ __forceinline__ bool pers_in_front(const uint32_t* front, int32_t u) {
+    return (__ldcg(front + (u >> 5)) >> (u & 31)) & 1u;
+}
+
+__global__ void __launch_bounds__(kPersThreads) k_bfs_persistent(
+    const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
+    uint32_t* visited, uint32_t* f0, uint32_t* f1, int64_t words, int2* __restrict__ rec,
+    const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, Queue qa, Queue qb,
+    unsigned long long* cnt, int32_t* big, Ctl* ctl, LevelRec* lrec, GridBar grid) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+    const int64_t gwarp = gtid >> 5, nwarps = nthr >> 5;
+    const long long* cw = reinterpret_cast<const long long*>(ctl);
+    for (;;) {
+        // every thread derives the same step decision from the state of the last barrier
+        Ctl c;
+        {
+            long long* cp = reinterpret_cast<long long*>(&c);
+            for (int i = 0; i < (int)(sizeof(Ctl) / 8); ++i) cp[i] = __ldcg(cw + i);
+        }
+        const long long ts = gtimer();
+        const long long m_u = step_decide(c);
+        const int32_t lvl = c.d + 1;
+        const Queue qc = c.qsel ? qb : qa, qn = c.qsel ? qa : qb;
+        uint32_t* front = c.fsel ? f1 : f0;
+        uint32_t* next = c.fsel ? f0 : f1;
+        unsigned long long my_n = 0, my_mf = 0, my_insp = 0, my_scan = 0;
+        if (c.dir == 0) {
+            // ---------------- top-down
+            if (!c.have_queue) {
+                b2q_body(front, words, 0, head, qc, cnt);
+                grid.sync();
+            }
+            int nbig = 0;
+            // small rows: warp per frontier vertex; big rows are listed for the grid
+            for (int64_t i = gwarp; i < c.n_f; i += nwarps) {
+                const int32_t u = __ldcg(qc.v + i);
+                const int32_t dg = __ldcg(qc.deg + i);
+                if (dg >= kPersBig) {
+                    if (lane == 0) big[atomicAdd(cnt + C_SCAN, 1ull)] = u;
+                    continue;
+                }
+                const int64_t b = __ldg(off + u);
+                const int32_t pu = pmap ? __ldg(pmap + u) : u;
+                for (int j0 = 0; j0 < dg; j0 += 32) {
+                    bool win = false;
+                    int32_t v = 0;
+                    if (j0 + lane < dg) {
+                        v = __ldg(adj + b + j0 + lane);
+                        const uint32_t bit = 1u << (v & 31);
+                        uint32_t* wp = visited + (v >> 5);
+                        if (!(__ldcg(wp) & bit)) win = !(atomicOr(wp, bit) & bit);
+                    }
+                    const unsigned m = __ballot_sync(kFull, win);
+                    if (m) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (win) {
+                            const int32_t vd = __ldg(head + v).y;
+                            queue_put(qn, base + __popc(m & lanemask_lt()), v, vd);
+                            rec[v] = make_int2(lvl, pu);
+                            my_mf += (unsigned long long)vd;
+                        }
+                    }
+                }
+            }
+            grid.sync();
+            nbig = (int)__ldcg(cnt + C_SCAN);
+            for (int k = 0; k < nbig; ++k) {   // big rows: the whole grid, arc per thread
+                const int32_t u = __ldcg(big + k);
+                const int64_t b = __ldg(off + u), e = __ldg(off + u + 1);
+                const int32_t pu = pmap ? __ldg(pmap + u) : u;
+                for (int64_t j0 = b + gtid - lane; j0 < e; j0 += nthr) {
+                    const int64_t j = j0 + lane;
+                    bool win = false;
+                    int32_t v = 0;
+                    if (j < e) {
+                        v = __ldg(adj + j);
+                        const uint32_t bit = 1u << (v & 31);
+                        uint32_t* wp = visited + (v >> 5);
+                        if (!(__ldcg(wp) & bit)) win = !(atomicOr(wp, bit) & bit);
+                    }
+                    const unsigned m = __ballot_sync(kFull, win);
+                    if (m) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (win) {
+                            const int32_t vd = __ldg(head + v).y;
+                            queue_put(qn, base + __popc(m & lanemask_lt()), v, vd);
+                            rec[v] = make_int2(lvl, pu);
+                            my_mf += (unsigned long long)vd;
+                        }
+                    }
+                }
+            }
+        } else {
+            // ---------------- bottom-up
+            if (c.have_queue) {
+                for (int64_t w = gtid; w < words; w += nthr) front[w] = 0u;
+                grid.sync();
+                q2b_body(qc.v, c.n_f, front);
+                grid.sync();
+            }
+            for (int64_t w = gwarp; w < words; w += nwarps) {
+                const uint32_t vis = __ldcg(visited + w);
+                bool hit = false;
+                if (!((vis >> lane) & 1u)) {
+                    const int64_t v = w * 32 + lane;
+                    const int2 hd = __ldg(head + v);
+                    if (hd.y > 0) {
+                        my_scan += 1;
+                        int32_t pu = -1;
+                        if (pers_in_front(front, hd.x)) {
+                            hit = true;
+                            my_insp += 1;
+                            pu = hpar ? __ldg(hpar + v) : hd.x;
+                        } else {
+                            const int64_t b = __ldg(off + v);
+                            int64_t j = 1;
+                            for (; j < hd.y; ++j) {
+                                const int32_t u = __ldg(adj + b + j);
+                                if (pers_in_front(front, u)) {
+                                    hit = true;
+                                    pu = pmap ? __ldg(pmap + u) : u;
+                                    break;
+                                }
+                            }
+                            my_insp += (unsigned long long)(hit ? j + 1 : hd.y);
+                        }
+                        if (hit) {
+                            rec[v] = make_int2(lvl, pu);
+                            my_mf += (unsigned long long)hd.y;
+                        }
+                    }
+                }
+                const unsigned nb = __ballot_sync(kFull, hit);
+                if (lane == 0) {
+                    next[w] = nb;
+                    if (nb) visited[w] = vis | nb;
+                    my_n += (unsigned long long)__popc(nb);
+                }
+            }
+        }
+        my_n = warp_sum_u64(my_n);
+        my_mf = warp_sum_u64(my_mf);
+        my_insp = warp_sum_u64(my_insp);
+        my_scan = warp_sum_u64(my_scan);
+        if (lane == 0) {
+            if (c.dir == 1 && my_n) atomicAdd(cnt + C_NEXT, my_n);
+            if (my_mf) atomicAdd(cnt + C_MF, my_mf);
+            if (my_insp) atomicAdd(cnt + C_INSP, my_insp);
+            if (c.dir == 1 && my_scan) atomicAdd(cnt + C_SCAN, my_scan);
+        }
+        grid.sync();
+        if (gtid == 0) {
+            LevelRec r{};
+            r.n_f = c.n_f;
+            r.m_f = c.m_f;
+            r.m_u = m_u;
+            r.dir = c.dir;
+            r.ts = ts;
+            r.k0 = ts;
+            const bool cont = step_finish(c, r, cnt);
+            r.k1 = r.te;
+            lrec[c.d - 1] = r;
+            c.done = cont ? 0 : 1;
+            *ctl = c;
+            for (int i = 0; i < 8; ++i) cnt[i] = 0;
+        }
+        grid.sync();
+        if (reinterpret_cast<const volatile Ctl*>(ctl)->done) break;
+    }
 }
 
 int grid_for(int64_t items, int threads, int per_sm = 8) {
@@ -1329,22 +1557,53 @@ void bfs_release_loop(bfs_graph_s* g) {
     g->h_ctl = g->h_lrec = nullptr;
 }
 
-// One search with the device-driven loop.  Returns false (nothing to report) if
-// the search ran past kGraphMaxLevels levels; the caller reruns it host-driven.
+// graphs up to this many arcs use the persistent kernel in auto mode (BFS_PERSIST_MAX_ARCS)
+static int64_t persist_max_arcs() {
+    const char* e = getenv("BFS_PERSIST_MAX_ARCS");
+    return e ? atoll(e) : (int64_t)1 << 22;
+}
+
+static int pers_blocks_per_sm() {
+    const char* e = getenv("BFS_PERSIST_BLOCKS");   // tuning only
+    return e ? std::max(1, atoi(e)) : 1;
+}
+
+// co-resident CTAs of the persistent kernel (cooperative launch limit)
+static int pers_grid() {
+    static const int gsz = [] {
+        int per = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bfs_persistent, kPersThreads, 0) != cudaSuccess ||
+            per < 1) {
+            cudaGetLastError();
+            per = 1;
+        }
+        // fewer CTAs make every grid barrier cheaper; small graphs need no more
+        return std::min(per, pers_blocks_per_sm()) * num_sms();
+    }();
+    return gsz;
+}
+
+// One search with the device-driven loop: the loop graph, or (persistent) the
+// one-kernel search.  Returns false (nothing to report) if the search ran past
+// kGraphMaxLevels levels; the caller reruns it host-driven.
 static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op, int32_t* parent_out,
-                          int32_t* depth_out) {
+                          int32_t* depth_out, bool persistent) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
+    if (persistent) {
+        if (!g->ctl.p) build_loop_graph(g);   // the state buffers (the graph itself stays unused)
+        if (!g->big.p) g->big.alloc((size_t)(g->arcs_local / kPersBig + 4), s);   // + 2 barrier words
+    }
     // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
     const std::vector<int> key{bu_long_setting(), bu_dense_setting()};
-    if (g->loop_exec && g->loop_key != key) {
+    if (!persistent && g->loop_exec && g->loop_key != key) {
         BFS_CUDA(cudaStreamSynchronize(s));
         cudaGraphExecDestroy(g->loop_exec);
         cudaGraphDestroy(g->loop_graph);
         g->loop_exec = nullptr;
         g->loop_graph = nullptr;
     }
-    if (!g->loop_exec) {
+    if (!persistent && !g->loop_exec) {
         build_loop_graph(g);
         g->loop_key = key;
     }
@@ -1358,7 +1617,23 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
                                                  g->n, g->arcs_global, kGraphMaxLevels);
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
-    BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
+    if (persistent) {
+        const int64_t words = words_of(nl);
+        const Queue qb{g->q1.p, g->qd1.p};
+        LevelRec* lrec = reinterpret_cast<LevelRec*>(g->lrec.p);
+        const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
+        const int32_t* hpar = g->reindexed ? g->hpar.p : nullptr;
+        unsigned long long* cntp = (unsigned long long*)g->cnt.p;
+        // barrier words live in the tail of the big-row list buffer; zeroed per search
+        unsigned* bar = reinterpret_cast<unsigned*>(g->big.p + g->big.count - 2);
+        BFS_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
+        k_bfs_persistent<<<pers_grid(), kPersThreads, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, g->front.p,
+                                                              g->next.p, words, g->rec.p, pmap, hpar, qa, qb, cntp,
+                                                              g->big.p, ctl, lrec, GridBar{bar, bar + 1});
+        BFS_CHECK_LAUNCH();
+    } else {
+        BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
+    }
     BFS_CUDA(cudaEventRecord(g->ev[3], s));
     int64_t launches = 1;
     if (od || op) {
@@ -1407,7 +1682,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             comp += L.kernel_ms;
         }
         g->levels.push_back(L);
-        launches += 2 + (R[d].dir == 0 ? 4 : 3);
+        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 4 : 3);
     }
     float ms = 0, ms_init = 0, ms_loop = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
@@ -1418,7 +1693,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     g->run.ms_compute = lt ? comp : ms_loop;
     g->run.levels = c.d;
     g->run.reached = c.reached;
-    g->run.kernel_launches = launches;
+    g->run.kernel_launches = launches + (persistent ? 1 : 0);
     g->last_root_l = c.root_i;
     g->run.component_edge_tuples = -1;
     return true;
@@ -1459,8 +1734,13 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         const char* e = getenv("BFS_HOST_LOOP");   // A/B experiments only
         return e && e[0] == '1';
     }();
-    if (!mg && g->nparts == 1 && !g->policy.host_loop && !env_host_loop) {
-        if (bfs_run_graph(g, root, od, op, parent_out, depth_out)) return;
+    // level loop: 0 auto (persistent kernel for small graphs, loop graph otherwise),
+    // 1 host, 2 loop graph, 3 persistent kernel; p ranks always host-driven
+    int loop = g->policy.loop;
+    if (env_host_loop) loop = 1;
+    if (loop == 0) loop = g->arcs_local <= persist_max_arcs() ? 3 : 2;
+    if (!mg && g->nparts == 1 && loop != 1) {
+        if (bfs_run_graph(g, root, od, op, parent_out, depth_out, loop == 3)) return;
         g->levels.clear();   // deeper than the graph's record capacity: host loop below
         g->run = bfs_run_stats{};
         g->run.root = root;

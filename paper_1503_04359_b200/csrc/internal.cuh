@@ -172,6 +172,7 @@ struct bfs_graph_s {
     int64_t* h_lrec = nullptr;
 
     bfs_policy policy{0, 15, 18, 0, 0, 0};
+    bfsb::DevBuf<int32_t> big;       // persistent kernel: big frontier rows of a top-down step
     std::vector<bfs_level_stats> levels;
     bfs_run_stats run{};
     int64_t last_root_l = 0;

@@ -22,8 +22,10 @@ pytestmark = pytest.mark.gpu
 POLICIES = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=2, bu_from_level=0),
             dict(mode=0, alpha=2, beta=4), dict(mode=0, alpha=100, beta=2),
             dict(mode=3, alpha=500, beta=3), dict(mode=3, alpha=50, beta=1),
-            # the host-driven level loop (default on one GPU: the device-driven graph loop)
-            dict(mode=0, host_loop=True), dict(mode=3, alpha=500, beta=3, host_loop=True)]
+            # every level loop (auto picks the persistent kernel for these small graphs)
+            dict(mode=0, loop="host"), dict(mode=3, alpha=500, beta=3, loop="host"),
+            dict(mode=0, loop="graph"), dict(mode=2, bu_from_level=1, loop="graph"),
+            dict(mode=3, alpha=500, beta=3, loop="graph"), dict(mode=1, loop="graph")]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -246,34 +248,40 @@ def test_repeated_runs_and_stream():
 
 
 def test_deep_search_falls_back_to_host_loop():
-    """A path of 5000 vertices needs 5000 steps: more than the device loop's record
+    """A path of 5000 vertices needs 5000 steps: more than the device loops' record
     capacity (4096), so the search is rerun host-driven; outputs and counters exact."""
     n, uv = graphs.path(5000)
     ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
     g = pkg.Graph.from_edges(uv, n)
-    for pol in (dict(mode=0), dict(mode=1)):
+    for pol in (dict(mode=0), dict(mode=1), dict(mode=0, loop="graph")):
         run, levels = _check_run(g, ref, 0, pol, uv)
         assert run["levels"] == 5000
     g.close()
 
 
-def test_graph_and_host_loops_agree_kronecker():
-    """Device-driven and host-driven level loops give identical outputs and step records."""
+@pytest.mark.parametrize("reindex", [False, True])
+def test_all_loops_agree_kronecker(reindex):
+    """Persistent kernel, loop graph and host loop give identical outputs and step records."""
     uv, ref = oracle.kron_graph(14, 16, 11)
-    g = pkg.Graph.kronecker(14, 16, 11)
+    g = pkg.Graph.kronecker(14, 16, 11, opts=pkg.default_opts(reindex_by_degree=reindex))
     for r in g.sample_roots(14, 11, 6):
         out = []
-        for host in (False, True):
-            g.set_policy(mode=0, alpha=30, beta=24, host_loop=host, level_times=True)
+        for loop in ("persistent", "graph", "host"):
+            g.set_policy(mode=0, alpha=30, beta=24, loop=loop, level_times=True)
             parent, depth = g.run(int(r))
             run, levels = g.stats()
             out.append((parent.cpu().numpy(), depth.cpu().numpy(), run, levels))
             assert all(lv["kernel_ms"] >= 0 and lv["ms"] > 0 for lv in levels)
-        assert np.array_equal(out[0][1], out[1][1])
-        for k in ("direction", "frontier", "discovered", "m_f", "m_u", "inspections", "scanned"):
-            assert [lv[k] for lv in out[0][3]] == [lv[k] for lv in out[1][3]], k
-        assert out[0][2]["reached"] == out[1][2]["reached"]
-        assert out[0][2]["component_edge_tuples"] == out[1][2]["component_edge_tuples"]
+        want, _ = oracle.bfs(ref, int(r)) if not reindex else (None, None)
+        for o in out[1:]:
+            assert np.array_equal(out[0][1], o[1])
+            for k in ("direction", "frontier", "discovered", "m_f", "m_u", "inspections", "scanned"):
+                assert [lv[k] for lv in out[0][3]] == [lv[k] for lv in o[3]], k
+            assert out[0][2]["reached"] == o[2]["reached"]
+            assert out[0][2]["component_edge_tuples"] == o[2]["component_edge_tuples"]
+        if want is not None:
+            assert np.array_equal(out[0][1], want)
+            assert not oracle.validate(ref, int(r), out[0][1], out[0][0], ref_depth=want)
     g.close()
 
 

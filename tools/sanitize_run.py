@@ -18,7 +18,7 @@ rng = np.random.default_rng(0)
 for opts in (pkg.default_opts(), pkg.default_opts(reindex_by_degree=True), pkg.default_opts(sort_rows=2),
              pkg.default_opts(False, False, False, 1)):
     g = pkg.Graph.kronecker(11, 16, 3, opts=opts)
-    for pol in (dict(mode=0), dict(mode=0, host_loop=True), dict(mode=1), dict(mode=2, bu_from_level=0),
+    for pol in (dict(mode=0), dict(mode=0, loop="host"), dict(mode=0, loop="graph"), dict(mode=1), dict(mode=2, bu_from_level=0),
                 dict(mode=3, alpha=500, beta=2)):
         g.set_policy(**pol)
         for r in g.sample_roots(11, 3, 3):
