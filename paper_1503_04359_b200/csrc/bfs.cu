@@ -1342,6 +1342,22 @@ int grid_for(int64_t items, int threads, int per_sm = 8) {
     return (int)std::max<int64_t>(1, std::min(b, cap));
 }
 
+// Bitmap words a search touches.  With the degree reindex every vertex >= n_active is
+// isolated: its visited bit is its skip bit forever (no step writes it), it is never a
+// frontier vertex, so the steps, conversions and the per-search visited reset cover
+// [0, n_active) only -- after one full reset.
+static bool active_range(const bfs_graph_s* g) {
+    return g->reindexed && !(g->comm && g->comm->nranks > 1) && g->nparts == 1;
+}
+static int64_t loop_words(const bfs_graph_s* g) {
+    return active_range(g) ? words_of(g->n_active) : words_of(g->nl());
+}
+static int64_t reset_words(bfs_graph_s* g) {
+    const int64_t pw = (active_range(g) && g->visited_tail_ok) ? padded_words(g->n_active) : padded_words(g->nl());
+    g->visited_tail_ok = true;
+    return pw;
+}
+
 // CTAs of the top-down kernel that are resident at once: its chunk loop is
 // grid-strided, so a grid larger than one wave would leave a straggling second wave
 template <bool kMulti>
@@ -1496,7 +1512,7 @@ static cudaGraph_t add_cond(cudaGraph_t G, const std::vector<cudaGraphNode_t>& d
 static void build_loop_graph(bfs_graph_s* g) {
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
-    const int64_t words = words_of(nl);
+    const int64_t words = loop_words(g);
     if (!g->ctl.p) {
         g->ctl.alloc(sizeof(Ctl) / 8, s);
         g->lrec.alloc((size_t)kGraphMaxLevels * sizeof(LevelRec) / 8, s);
@@ -1609,7 +1625,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     }
     Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
     const Queue qa{g->q0.p, g->qd0.p};
-    const int64_t pw = padded_words(nl);
+    const int64_t pw = reset_words(g);
     const bool lt = g->policy.level_times != 0;
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
     k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
@@ -1618,7 +1634,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
     if (persistent) {
-        const int64_t words = words_of(nl);
+        const int64_t words = loop_words(g);
         const Queue qb{g->q1.p, g->qd1.p};
         LevelRec* lrec = reinterpret_cast<LevelRec*>(g->lrec.p);
         const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
@@ -1766,7 +1782,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     }
 
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
-    const int64_t pw = padded_words(nl);
+    const int64_t pw = reset_words(g);
     Queue qcur{g->q0.p, g->qd0.p};
     Queue qnxt{g->q1.p, g->qd1.p};
     k_init<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root_l, (int32_t)root_i, rec, (int32_t)root, qcur,
@@ -1786,7 +1802,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     int64_t prev_nf = 0, seen = 0, reached = 0;
     int64_t m_fc = h[C_GLOBAL + C_COORD], bu_done = 0;  // policy 3: coordinator m_f, BU steps taken
     bool returned = false;
-    const int64_t words = words_of(nl);
+    const int64_t words = loop_words(g);
     const size_t slice_bytes = mg ? (size_t)(g->nb / 8) : 0;
     uint64_t nvl_total = 0;
     std::vector<size_t> sendb(p), recvb(p);

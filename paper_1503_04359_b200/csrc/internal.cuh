@@ -137,6 +137,7 @@ struct bfs_graph_s {
     // reindex (identity when absent)
     bool reindexed = false;
     int64_t n_active = 0;            // reindexed: labels >= n_active are isolated
+    bool visited_tail_ok = false;    // visited words past n_active hold their skip bits
     bfsb::DevBuf<int32_t> label;    // [n] original -> internal
     bfsb::DevBuf<int32_t> ilabel;   // [n] internal -> original
 
