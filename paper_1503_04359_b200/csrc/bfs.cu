@@ -54,6 +54,12 @@ __device__ __forceinline__ unsigned lanemask_lt() {
     return r;
 }
 
+__device__ __forceinline__ uint32_t ld_ca(const uint32_t* p) {
+    uint32_t r;
+    asm volatile("ld.global.ca.u32 %0, [%1];" : "=r"(r) : "l"(p));
+    return r;
+}
+
 __device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long x) {
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(kFull, x, d);
@@ -162,7 +168,7 @@ struct Remote {          // p > 1 only
 //   C  winners write depth/parent and stage v in shared memory; one atomicAdd per
 //      CTA chunk on the global queue tail, then a coalesced copy of the stage.
 template <bool kMulti>
-__global__ void __launch_bounds__(kTdThreads, 5)
+__global__ void __launch_bounds__(kTdThreads, 4)
 k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t* __restrict__ starts,
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
@@ -207,36 +213,57 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         }
         __syncthreads();
         int32_t v[kTdItems], u[kTdItems];
-        // A: targets
-#pragma unroll
-        for (int j = 0; j < kTdItems; ++j) {
-            const int64_t e = e0 + (int64_t)j * kTdThreads + threadIdx.x;
-            v[j] = -1;
-            u[j] = 0;
-            if (e < e1) {
-                int64_t beg, pre;
+        // A: targets.  Thread t takes kTdItems CONSECUTIVE arcs: one binary search for
+        // the first, then a linear advance; the arcs of a row are sorted, so a thread's
+        // targets are close together and its visited probes mostly share a sector (L1).
+        {
+            const int64_t et = e0 + (int64_t)threadIdx.x * kTdItems;
+            int64_t a = 0;
+            if (et < e1) {
                 if (fits) {
-                    int a = 0, b = (int)cntv - 1;
-                    while (a < b) {
-                        const int mid = (a + b + 1) >> 1;
-                        if (s_pre[mid] <= e) a = mid;
-                        else b = mid - 1;
+                    int lo_ = 0, hi_ = (int)cntv - 1;
+                    while (lo_ < hi_) {
+                        const int mid = (lo_ + hi_ + 1) >> 1;
+                        if (s_pre[mid] <= et) lo_ = mid;
+                        else hi_ = mid - 1;
                     }
-                    u[j] = s_u[a];
-                    beg = s_beg[a];
-                    pre = s_pre[a];
+                    a = lo_;
                 } else {
-                    int64_t a = i0, b = F - 1;
-                    while (a < b) {
-                        const int64_t mid = (a + b + 1) >> 1;
-                        if (prefix[mid] <= e) a = mid;
-                        else b = mid - 1;
+                    int64_t lo_ = i0, hi_ = F - 1;
+                    while (lo_ < hi_) {
+                        const int64_t mid = (lo_ + hi_ + 1) >> 1;
+                        if (prefix[mid] <= et) lo_ = mid;
+                        else hi_ = mid - 1;
                     }
-                    u[j] = q.v[a];
-                    beg = off[u[j] - lo];
-                    pre = prefix[a];
+                    a = lo_;
                 }
-                v[j] = __ldcs(adj + beg + (e - pre));   // streamed once: evict-first
+            }
+            int64_t pre = 0, nxt = 0, beg = 0;
+            int32_t uu = 0;
+            if (et < e1) {
+                if (fits) {
+                    pre = s_pre[a]; nxt = s_pre[a + 1]; beg = s_beg[a]; uu = s_u[a];
+                } else {
+                    pre = prefix[a]; nxt = prefix[a + 1]; uu = q.v[a]; beg = off[uu - lo];
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kTdItems; ++j) {
+                const int64_t e = et + j;
+                v[j] = -1;
+                u[j] = 0;
+                if (e < e1) {
+                    while (e >= nxt) {   // the next frontier vertex (degree >= 1: one step each)
+                        ++a;
+                        if (fits) {
+                            pre = s_pre[a]; nxt = s_pre[a + 1]; beg = s_beg[a]; uu = s_u[a];
+                        } else {
+                            pre = prefix[a]; nxt = prefix[a + 1]; uu = q.v[a]; beg = off[uu - lo];
+                        }
+                    }
+                    u[j] = uu;
+                    v[j] = __ldg(adj + beg + (e - pre));
+                }
             }
         }
         // B: probe, then claim.  Owned targets in `visited`, remote ones in `seen`.
@@ -248,7 +275,9 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
             own[j] = !kMulti || (v[j] >= lo && v[j] < hi);
             wp[j] = nullptr;
             if (v[j] >= 0) wp[j] = own[j] ? visited + ((v[j] - lo) >> 5) : rm.seen + (v[j] >> 5);
-            wv[j] = wp[j] ? __ldcg(wp[j]) : kFull;
+            // L1-cached probe: visited/seen bits only ever go 0 -> 1 during a step, so a
+            // stale word can only send a claim to the atomicOr, which decides correctly
+            wv[j] = wp[j] ? ld_ca(wp[j]) : kFull;
         }
         bool win[kTdItems];
 #pragma unroll
