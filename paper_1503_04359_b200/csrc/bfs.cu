@@ -387,7 +387,7 @@ __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int
     return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
 
-constexpr int kBuLongDefault = 8;
+constexpr int kBuLongDefault = 64;   // B200 sweep: 8 -> 64 is +1%; the warp path stays for hub rows
 // lane-serial probes before a row is handed to the whole warp (BFS_BU_LONG: tuning only)
 static int bu_long_setting() {
     const char* e = getenv("BFS_BU_LONG");
