@@ -298,3 +298,50 @@ def test_edge_list_file_ingestion(tmp_path):
     for root in (0, int(np.argmax(ref.degree()))):
         _check_run(g, ref, root, dict(mode=0), uv)
     g.close()
+
+
+def _check_outputs(g, ref, root, policy):
+    """depth == oracle, parents valid, reached count -- label-order independent checks."""
+    g.set_policy(**policy)
+    parent, depth = g.run(int(root))
+    d = depth.cpu().numpy()
+    p = parent.cpu().numpy()
+    want, _ = oracle.bfs(ref, int(root))
+    assert np.array_equal(d, want), (root, policy, np.nonzero(d != want)[0][:8])
+    assert not oracle.validate(ref, int(root), d, p, ref_depth=want)
+    run, levels = g.stats()
+    assert run["reached"] == int((want >= 0).sum())
+    assert sum(lv["frontier"] for lv in levels) == run["reached"]
+
+
+def _degenerate_cases():
+    rng = np.random.default_rng(5)
+    e0 = np.zeros((0, 2), np.int32)
+    loops = np.array([[v, v] for v in range(0, 50, 2)], np.int32)
+    n_hub, hub = graphs.star(5000)                       # a row longer than every shared-memory path
+    hub = np.concatenate([hub, rng.integers(1, n_hub, size=(3000, 2)).astype(np.int32)])
+    n_u, uni = graphs.disjoint_union(graphs.path(7), graphs.clique(5), graphs.star(33))
+    return {
+        "single": (1, e0), "edgeless": (1000, e0), "self_loops_only": (50, loops),
+        "ragged33": graphs.path(33), "ragged1025": graphs.random_edges(1025, 4000, 7),
+        "ragged4097": graphs.random_edges(4097, 30000, 8), "hub5000": (n_hub, hub),
+        "isolated_tail": (n_u + 77, uni),                # 77 isolated vertices after the components
+    }
+
+
+@pytest.mark.parametrize("loop", ["persistent", "graph", "host"])
+@pytest.mark.parametrize("reindex", [False, True])
+def test_degenerate_and_ragged_graphs(loop, reindex):
+    """Empty, edgeless, self-loop-only and ragged-size graphs, a long hub row, isolated roots:
+    every level loop, with and without the degree reindex (isolated vertices last)."""
+    for name, (n, uv) in _degenerate_cases().items():
+        g = pkg.Graph.from_edges(uv, n, opts=pkg.default_opts(reindex_by_degree=reindex))
+        ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+        deg = ref.degree()
+        roots = {0, n - 1, int(np.argmax(deg))}
+        if (deg == 0).any():
+            roots.add(int(np.nonzero(deg == 0)[0][-1]))   # an isolated root
+        for root in sorted(roots):
+            for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
+                _check_outputs(g, ref, root, dict(loop=loop, **pol))
+        g.close()
