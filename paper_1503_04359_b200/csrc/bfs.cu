@@ -418,12 +418,13 @@ static int bu_dense_setting() {
 //      hitting lane is the first frontier neighbour in row order);
 //   5. the 32 next words are assembled in shared memory and stored coalesced.
 constexpr int kBuWarps = 8;
+constexpr int kBuCtas = 4;     // resident CTAs per SM (launch bound and grid; 5 spills: -10%)
 constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (one aligned vector load) and probes per round
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
-__global__ void __launch_bounds__(kBuWarps * 32, 4)
+__global__ void __launch_bounds__(kBuWarps * 32, 6)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
@@ -1583,7 +1584,7 @@ static void build_loop_graph(bfs_graph_s* g) {
     cudaGraphNode_t u1 = add_kernel(U, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
     cudaGraphNode_t u2 = add_kernel(U, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
     const int64_t nbatches = (words + 31) / 32;
-    const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, 4);
+    const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
     const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
     add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
                g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
@@ -2012,7 +2013,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             l2_window(g, front, g->front.bytes());
             const int64_t nbatches = (words + 31) / 32;
-            const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, 4);
+            const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
                                                          pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
