@@ -161,3 +161,24 @@ def test_degree_row_order_multi(p):
     for r in roots:
         _check(gs, ref, r, dict(mode=0), uv)
     _close(comms, gs)
+
+
+def test_nccl_bootstrap_single_rank():
+    """The NCCL backend (dlopen of torch's libnccl, unique id, CommInitRank) on the one GPU
+    a box has: a one-rank communicator builds the graph and searches like no communicator."""
+    import torch
+    torch.cuda.set_device(0)
+    uid = pkg.bfs_comm_unique_id()
+    assert len(uid) == 128 and any(uid)
+    comm = pkg.bfs_comm_create(1, 0, uid, 0)
+    scale, seed = 12, 4
+    uv, ref = oracle.kron_graph(scale, 16, seed)
+    g = pkg.Graph.kronecker(scale, 16, seed, comm=comm)
+    assert (g.local_begin, g.local_end) == (0, ref.n)
+    for r in g.sample_roots(scale, seed, 3):
+        parent, depth = g.run(int(r))
+        want, _ = oracle.bfs(ref, int(r))
+        assert np.array_equal(depth.cpu().numpy(), want)
+        assert not oracle.validate(ref, int(r), depth.cpu().numpy(), parent.cpu().numpy(), ref_depth=want)
+    g.close()
+    pkg.bfs_comm_destroy(comm)
