@@ -424,7 +424,7 @@ constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (one aligned vector load) and probes per round
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
-__global__ void __launch_bounds__(kBuWarps * 32, 6)
+__global__ void __launch_bounds__(kBuWarps * 32, kBuCtas)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
