@@ -65,3 +65,34 @@ def test_errors_are_reported_not_swallowed(so):
     assert st == 1 and b"NULL" in pkg.lib().bfs_last_error()
     with pytest.raises(pkg.BfsError):
         pkg.bfs_graph_create_kronecker(8)   # no device here -> BFS_ERR_CUDA, never a CPU fallback
+
+
+def test_hot_kernel_resource_budget(so):
+    """Guard the measured occupancy design points: the bottom-up and
+    top-down kernels keep 4 resident 256-thread CTAs per SM (64 registers) with at most a
+    trivial spill -- a stray launch-bound edit once cost 10%."""
+    import shutil
+    tool = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(tool):
+        pytest.skip("cuobjdump not available")
+    out = subprocess.run([tool, "-res-usage", so], capture_output=True, text=True).stdout
+    usage = {}
+    name = None
+    for line in out.splitlines():
+        m = re.search(r"Function (\S+):", line)
+        if m:
+            name = m.group(1)
+            continue
+        m = re.search(r"REG:(\d+) STACK:(\d+)", line)
+        if m and name:
+            usage[name] = (int(m.group(1)), int(m.group(2)))
+            name = None
+    bu = [v for k, v in usage.items() if "k_bu_batch" in k]
+    td = [v for k, v in usage.items() if "k_td_expandILb0" in k]      # the single-partition variant
+    td_multi = [v for k, v in usage.items() if "k_td_expandILb1" in k]
+    assert bu and td and td_multi
+    for reg, stack in bu + td:
+        assert 48 < reg <= 64, (reg, stack)      # 4 CTAs x 256 threads per SM, not fewer registers
+        assert stack <= 16, (reg, stack)         # no real spilling
+    for reg, stack in td_multi:                  # p ranks: the remote-claim path adds a small spill
+        assert 48 < reg <= 64 and stack <= 64, (reg, stack)
