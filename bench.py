@@ -258,10 +258,6 @@ def main():
 
     cfg = CONFIGS[args.config]
     stream = torch.cuda.Stream()
-    if ws > 1 and args.reindex:
-        # the degree reindex is single-partition in this build: on p
-        # ranks the same section 3.4 locality comes from degree-ordered rows (sort_rows 2)
-        args.reindex, args.rows = 0, "degree"
     opts = pkg.default_opts(reindex_by_degree=bool(args.reindex), sort_rows=2 if args.rows == "degree" else 1)
     g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], opts=opts, comm=comm, stream=stream)
     build_ms = g.build_ms

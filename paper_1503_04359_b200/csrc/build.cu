@@ -169,6 +169,32 @@ __global__ void k_head_parent(const int2* head, const int32_t* ilabel, int64_t n
     }
 }
 
+// Degree reindex on p ranks (SURVEY 8(e) partitioning; the oracle's orc_degree_reindex):
+// position k of the (degree desc, ID asc) order is dealt round-robin, internal label
+// (k % p) * nb + k / p (nb = n / p), so every rank owns an equal share of the hubs and
+// its own vertices in degree order (isolated ones last).
+__global__ void k_deal(const int32_t* order, int64_t n, int p, int64_t nb, int32_t* label, int32_t* ilabel) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = order[k];
+        const int64_t id = (k % p) * nb + k / p;
+        label[v] = (int32_t)id;
+        ilabel[id] = v;
+    }
+}
+// internal label <-> degree position (rows are kept in global degree order)
+__global__ void k_ids_to_pos(int32_t* adj, int64_t arcs, int p, int64_t nb) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < arcs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t id = adj[j];
+        adj[j] = (int32_t)((id % nb) * p + id / nb);
+    }
+}
+__global__ void k_pos_to_ids(int32_t* adj, int64_t arcs, int p, int64_t nb) {
+    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < arcs; j += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = adj[j];
+        adj[j] = (int32_t)((k % p) * nb + k / p);
+    }
+}
+
 // degree-order helpers: key = maxdeg - deg (ascending key = descending degree)
 __global__ void k_local_degree(const int64_t* off, int64_t nl, int32_t* deg) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x)
@@ -769,9 +795,35 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         g->adj.reset();
         g->off.reset();
         g->deg_raw.reset();
-        g->label = std::move(rank);
-        g->ilabel = std::move(order);
+        const bool mg = g->comm && g->comm->nranks > 1;
+        const int p = mg ? g->comm->nranks : 1;
+        if (mg) {
+            // round-robin deal of the degree positions (nb = n / p, checked by the ABI)
+            DevBuf<int32_t> lab, ilab;
+            lab.alloc((size_t)g->n, s);
+            ilab.alloc((size_t)g->n, s);
+            k_deal<<<grid_for(g->n, 256), 256, 0, s>>>(order.p, g->n, p, g->nb, lab.p, ilab.p);
+            BFS_CHECK_LAUNCH();
+            rank.reset();
+            order.reset();
+            g->label = std::move(lab);
+            g->ilabel = std::move(ilab);
+        } else {
+            g->label = std::move(rank);
+            g->ilabel = std::move(order);
+        }
         build_pass(g, d, g->label.p);
+        if (mg) {
+            // rows in global degree order, not in the order of the dealt labels
+            k_ids_to_pos<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, p, g->nb);
+            BFS_CHECK_LAUNCH();
+            const bfs_build_opts keep = g->opts;
+            g->opts = bfs_build_opts{0, 0, 0, 1};
+            sort_and_compact(g);
+            g->opts = keep;
+            k_pos_to_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, p, g->nb);
+            BFS_CHECK_LAUNCH();
+        }
         g->reindexed = true;
         // isolated vertices are last in (degree desc, ID asc) order
         DevBuf<unsigned long long> cntz;

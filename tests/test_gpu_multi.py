@@ -182,3 +182,58 @@ def test_nccl_bootstrap_single_rank():
         assert not oracle.validate(ref, int(r), depth.cpu().numpy(), parent.cpu().numpy(), ref_depth=want)
     g.close()
     pkg.bfs_comm_destroy(comm)
+
+
+@pytest.mark.parametrize("p", [2, 4, 8])
+def test_degree_reindex_multi(p):
+    """Degree reindex on p ranks: degree positions dealt round-robin (the
+    oracle's degree_reindex(g, p)), rows in global degree order, outputs gathered back to
+    the ranks owning the ORIGINAL labels by the final aggregation step."""
+    scale, seed = 14, 5
+    uv, ref = oracle.kron_graph(scale, 16, seed)
+    lab, pos = oracle.degree_reindex(ref, p)
+    rel = oracle.relabel_csr(ref, lab, pos)
+    inv = np.empty_like(lab)
+    inv[lab] = np.arange(ref.n)
+    opts = pkg.default_opts(reindex_by_degree=True)
+    comms, gs = _build(p, lambda c, s: pkg.Graph.kronecker(scale, 16, seed, comm=c, stream=s, opts=opts))
+    for g in gs:   # every rank holds exactly the oracle's relabeled rows of its range
+        off, adj = g.export_csr()
+        lo, hi = g.local_begin, g.local_end
+        assert np.array_equal(off.cpu().numpy(), rel.offsets[lo:hi + 1] - rel.offsets[lo])
+        assert np.array_equal(adj.cpu().numpy(), rel.adj[rel.offsets[lo]:rel.offsets[hi]])
+    roots = pkg.run_ranks(lambda r: gs[r].sample_roots(scale, seed, 6), p)
+    assert np.array_equal(roots[0], oracle.sample_roots(ref, scale, seed, 6))
+    nb = gs[0].local_end
+    pols = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=3, alpha=500, beta=3)]
+    for i, r in enumerate(roots[0]):
+        pol = pols[i % len(pols)]
+        parent, depth, runs, levels = _run_all(gs, r, pol)
+        want, _ = oracle.bfs(ref, int(r))
+        assert np.array_equal(depth, want), np.nonzero(depth != want)[0][:10]
+        assert not oracle.validate(ref, int(r), depth, parent, ref_depth=want)
+        want_int = np.empty_like(want)
+        want_int[lab] = want
+        emu = oracle.do_emulate(rel, want_int, alpha=pol.get("alpha", 15), beta=pol.get("beta", 18),
+                                policy=pol["mode"], bu_from=pol.get("bu_from_level", 0), want_bu_parent=True,
+                                coord_hi=nb)
+        for lv in levels:
+            for key, lk in (("dir", "direction"), ("n_f", "frontier"), ("discovered", "discovered"),
+                            ("m_f", "m_f"), ("m_u", "m_u"), ("insp", "inspections")):
+                assert [x[lk] for x in lv] == emu[key].tolist(), key
+        bu = np.nonzero(emu["bu_parent"] >= 0)[0]            # internal labels found bottom-up
+        assert np.array_equal(parent[inv[bu]], inv[emu["bu_parent"][bu]])
+        for run in runs:
+            assert run["reached"] == int((want >= 0).sum())
+            assert run["component_edge_tuples"] == oracle.component_tuples(uv, want)
+            assert run["ms_aggregate"] > 0
+    _close(comms, gs)
+
+
+def test_degree_reindex_multi_needs_exact_deal():
+    comms = pkg.bfs_comm_create_local(3, 0)
+    with pytest.raises(pkg.BfsError, match="divisible"):
+        pkg.run_ranks(lambda r: pkg.Graph.kronecker(10, 16, 1, comm=comms[r],
+                                                    opts=pkg.default_opts(reindex_by_degree=True)), 3)
+    for c in comms:
+        pkg.bfs_comm_destroy(c)

@@ -34,6 +34,17 @@ g.run(0)
 h = np.empty(n, np.int32)
 pkg.bfs_run(g.h, 0, h, None)
 g.close()
+# multi-partition with the degree reindex and the final aggregation (local transport)
+comms_r = pkg.bfs_comm_create_local(2, 0)
+gr = pkg.run_ranks(lambda r: pkg.Graph.kronecker(10, 16, 2, comm=comms_r[r], stream=torch.cuda.Stream(),
+                                                 opts=pkg.default_opts(reindex_by_degree=True)), 2)
+def go_r(r):
+    torch.cuda.set_device(0)
+    gr[r].run(5)
+    return gr[r].stats()
+pkg.run_ranks(go_r, 2)
+for x in gr:
+    x.close()
 # multi-partition (local transport)
 comms = pkg.bfs_comm_create_local(3, 0)
 gs = pkg.run_ranks(lambda r: pkg.Graph.kronecker(10, 16, 2, comm=comms[r], stream=torch.cuda.Stream()), 3)
