@@ -40,6 +40,8 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "k29"
 METRIC = "Graph500 harmonic-mean GTEPS (64 roots)"
+# the paper's rate for the same metric and workload (Scale29, 2x Xeon + 2x K40)
+PAPER_GTEPS = {"k29": 17.3}
 ROOTS = 64
 # random 4-byte L2 probes per second on B200 (measured: profiles/r01_l2_probe_micro.txt)
 L2_PROBE_PEAK = 270.0
@@ -368,7 +370,9 @@ def main():
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 4), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "strong",
+        "vs_baseline": round(value / PAPER_GTEPS[args.config], 2) if args.config in PAPER_GTEPS else None,
+        "dtype": "int32", "data": "synthetic",
         "config": {"workload": cfg["name"], "scale": cfg["scale"], "edgefactor": cfg["ef"], "seed": cfg["seed"],
                    "roots": len(roots), "policy": args.policy,
                    "alpha": args.paper_alpha if args.policy == "paper" else args.alpha,
