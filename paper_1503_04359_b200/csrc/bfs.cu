@@ -346,12 +346,17 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
         const int32_t* hpar = g->reindexed ? g->hpar.p : nullptr;
         unsigned long long* cntp = (unsigned long long*)g->cnt.p;
-        // barrier words live in the tail of the big-row list buffer; zeroed per search
+        // barrier words live in the tail of the big-row list buffer; the three counter sets
+        // start at zero except what k_init_dev put in set 0
         unsigned* bar = reinterpret_cast<unsigned*>(g->big.p + g->big.count - 2);
         BFS_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
+        if (!g->pcnt.p) g->pcnt.alloc(48, s);
+        BFS_CUDA(cudaMemsetAsync(g->pcnt.p, 0, 48 * sizeof(int64_t), s));
+        BFS_CUDA(cudaMemcpyAsync(g->pcnt.p, cntp, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
         k_bfs_persistent<<<pers_grid(), kPersThreads, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, g->front.p,
-                                                              g->next.p, words, g->rec.p, pmap, hpar, qa, qb, cntp,
-                                                              g->big.p, ctl, lrec, GridBar{bar, bar + 1});
+                                                              g->next.p, words, g->rec.p, pmap, hpar, qa, qb,
+                                                              (unsigned long long*)g->pcnt.p, g->big.p, ctl, lrec,
+                                                              GridBar{bar, bar + 1});
         BFS_CHECK_LAUNCH();
     } else {
         BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));

@@ -277,19 +277,24 @@ __global__ void __launch_bounds__(kPersThreads) k_bfs_persistent(
     const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
     uint32_t* visited, uint32_t* f0, uint32_t* f1, int64_t words, int2* __restrict__ rec,
     const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, Queue qa, Queue qb,
-    unsigned long long* cnt, int32_t* big, Ctl* ctl, LevelRec* lrec, GridBar grid) {
+    unsigned long long* cnt3, int32_t* big, Ctl* ctl, LevelRec* lrec, GridBar grid) {
+    // One grid barrier per level: the counters are triple-buffered (level d accumulates
+    // into set d % 3, zeroed by thread 0 two levels ahead), and every thread rolls its own
+    // copy of the loop state from them after the barrier (the same arithmetic on the
+    // same numbers, so all copies agree); thread 0 keeps the step records and publishes
+    // the final state.
     const int lane = threadIdx.x & 31;
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5, nwarps = nthr >> 5;
-    const long long* cw = reinterpret_cast<const long long*>(ctl);
+    Ctl c;
+    {
+        const long long* cw = reinterpret_cast<const long long*>(ctl);
+        long long* cp = reinterpret_cast<long long*>(&c);
+        for (int i = 0; i < (int)(sizeof(Ctl) / 8); ++i) cp[i] = __ldcg(cw + i);
+    }
     for (;;) {
-        // every thread derives the same step decision from the state of the last barrier
-        Ctl c;
-        {
-            long long* cp = reinterpret_cast<long long*>(&c);
-            for (int i = 0; i < (int)(sizeof(Ctl) / 8); ++i) cp[i] = __ldcg(cw + i);
-        }
+        unsigned long long* cnt = cnt3 + 16 * (c.d % 3);
         const long long ts = gtimer();
         const long long m_u = step_decide(c);
         const int32_t lvl = c.d + 1;
@@ -426,23 +431,24 @@ __global__ void __launch_bounds__(kPersThreads) k_bfs_persistent(
             if (c.dir == 1 && my_scan) atomicAdd(cnt + C_SCAN, my_scan);
         }
         grid.sync();
+        unsigned long long cv[8];
+        for (int i = 0; i < 8; ++i) cv[i] = __ldcg(cnt + i);
+        LevelRec r{};
+        r.n_f = c.n_f;
+        r.m_f = c.m_f;
+        r.m_u = m_u;
+        r.dir = c.dir;
+        r.ts = ts;
+        r.k0 = ts;
+        const bool cont = step_finish(c, r, cv);
+        r.k1 = r.te;
         if (gtid == 0) {
-            LevelRec r{};
-            r.n_f = c.n_f;
-            r.m_f = c.m_f;
-            r.m_u = m_u;
-            r.dir = c.dir;
-            r.ts = ts;
-            r.k0 = ts;
-            const bool cont = step_finish(c, r, cnt);
-            r.k1 = r.te;
             lrec[c.d - 1] = r;
-            c.done = cont ? 0 : 1;
-            *ctl = c;
-            for (int i = 0; i < 8; ++i) cnt[i] = 0;
+            unsigned long long* z = cnt3 + 16 * ((c.d + 1) % 3);   // the set of level d + 2
+            for (int i = 0; i < 16; ++i) z[i] = 0;
+            if (!cont) *ctl = c;
         }
-        grid.sync();
-        if (reinterpret_cast<const volatile Ctl*>(ctl)->done) break;
+        if (!cont) break;
     }
 }
 

@@ -175,6 +175,7 @@ struct bfs_graph_s {
 
     bfs_policy policy{0, 15, 18, 0, 0, 0};
     bfsb::DevBuf<int32_t> big;       // persistent kernel: big frontier rows of a top-down step
+    bfsb::DevBuf<int64_t> pcnt;      // persistent kernel: three counter sets
     std::vector<bfs_level_stats> levels;
     bfs_run_stats run{};
     int64_t last_root_l = 0;
