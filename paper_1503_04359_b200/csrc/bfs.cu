@@ -64,6 +64,13 @@ static int64_t reset_words(bfs_graph_s* g) {
     return pw;
 }
 
+// top-down steps with at least this many arcs run claim-only + k_td_finish
+// (single partition; BFS_TD_CLAIM_MIN overrides: tuning only)
+static int64_t td_claim_min() {
+    const char* e = getenv("BFS_TD_CLAIM_MIN");
+    return e ? atoll(e) : (int64_t)1 << 26;
+}
+
 // CTAs of the top-down kernel that are resident at once: its chunk loop is
 // grid-strided, so a grid larger than one wave would leave a straggling second wave
 template <bool kMulti>
@@ -248,14 +255,17 @@ static void build_loop_graph(bfs_graph_s* g) {
     add_kernel(B, {n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
     // top-down body
     cudaGraphNode_t t1 = add_kernel(T, {}, k_td_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words, g->head.p, qa, qb,
-                                    cnt, tstate, g->tctr.p);
+                                    cnt, tstate, g->tctr.p, (const uint32_t*)g->visited.p);
     cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, (int64_t)0, g->prefix.p,
                                     tstate, g->tctr.p);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
                                     g->scratch64.p, ctl);
-    add_kernel(T, {t3}, k_td_expand<false>, dim3(td_resident_grid<false>()), dim3(kTdThreads), 0, qa, g->prefix.p, g->scratch64.p, (int64_t)0,
-               (int64_t)0, g->off.p, g->adj.p, g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo,
-               g->hi, Remote{}, ctl, lrec);
+    cudaGraphNode_t t4 = add_kernel(T, {t3}, k_td_expand<false>, dim3(td_resident_grid<false>()), dim3(kTdThreads), 0,
+                                    qa, g->prefix.p, g->scratch64.p, (int64_t)0, (int64_t)0, g->off.p, g->adj.p,
+                                    g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo, g->hi, Remote{},
+                                    ctl, lrec, -1);
+    add_kernel(T, {t4}, k_td_finish_dev, g8, t256, 0, ctl, (const uint32_t*)g->visited.p, g->front.p, g->next.p, words,
+               g->head.p, qa, qb, cnt);
     // bottom-up body
     cudaGraphNode_t u1 = add_kernel(U, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
     cudaGraphNode_t u2 = add_kernel(U, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
@@ -336,7 +346,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
     k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
                                                  g->rec.p, qa, g->head.p, (unsigned long long*)g->cnt.p, ctl, g->policy,
-                                                 g->n, g->arcs_global, kGraphMaxLevels);
+                                                 g->n, g->arcs_global, kGraphMaxLevels, td_claim_min());
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
     if (persistent) {
@@ -409,7 +419,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             comp += L.kernel_ms;
         }
         g->levels.push_back(L);
-        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 4 : 3);
+        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 5 : 3);
     }
     float ms = 0, ms_init = 0, ms_loop = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
@@ -507,6 +517,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     uint32_t* front = g->front.p;
     uint32_t* next = g->next.p;
     bool have_queue = true;
+    bool front_ok = false;   // `front` also holds the current frontier (after a claim-mode TD step)
     int dir = 0;  // 0 TD, 1 BU
     int64_t n_f = h[C_GLOBAL + C_NEXT], m_f = h[C_GLOBAL + C_MF];
     int64_t nf_loc = h[C_NEXT], mf_loc = h[C_MF];
@@ -558,6 +569,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 have_queue = true;
             }
             const int64_t E = mf_loc;
+            bool claim_mode = false;
+            front_ok = false;
             Remote rm{};
             if (mg) {
                 rm.nb = g->nb;
@@ -584,14 +597,28 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                                                                           nullptr);
                 BFS_CHECK_LAUNCH();
                 const int grid = (int)std::min<int64_t>(nchunks, mg ? td_resident_grid<true>() : td_resident_grid<false>());
-                if (mg)
+                // large single-partition steps: claims + records only, the winners' degrees
+                // and the next queue from k_td_finish in vertex order (visited snapshot in
+                // `next`, which becomes the next frontier bitmap)
+                claim_mode = !mg && E >= td_claim_min();
+                if (claim_mode) {
+                    BFS_CUDA(cudaMemcpyAsync(next, g->visited.p, (size_t)words * 4, cudaMemcpyDeviceToDevice, s));
+                    k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
+                                                                   g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
+                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr, 1);
+                    BFS_CHECK_LAUNCH();
+                    k_td_finish<<<grid_for(words * 32, 256), 256, 0, s>>>(g->visited.p, next, words, g->head.p, qnxt,
+                                                                         cnt);
+                    BFS_CHECK_LAUNCH();
+                    launches += 2;
+                } else if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
                                                                   g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt, d + 1,
-                                                                  g->lo, g->hi, rm, nullptr, nullptr);
+                                                                  g->lo, g->hi, rm, nullptr, nullptr, 0);
                 else
                     k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
                                                                    g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
-                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr);
+                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr, 0);
                 BFS_CHECK_LAUNCH();
                 launches += 2;
             }
@@ -626,6 +653,10 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 }
             }
             std::swap(qcur, qnxt);
+            if (claim_mode) {
+                std::swap(front, next);   // the next frontier as a bitmap too: BU needs no q2b
+                front_ok = true;
+            }
             insp = E;
             scanned = nf_loc;
         } else {
@@ -677,15 +708,16 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 }
                 have_queue = false;
             } else {
-                if (have_queue) {
+                if (have_queue && !front_ok) {
                     BFS_CUDA(cudaMemsetAsync(front + (g->lo >> 5), 0, (size_t)words_of(nl) * 4, s));
                     if (nf_loc) {
                         k_q2b<<<grid_for(nf_loc, 256), 256, 0, s>>>(qcur.v, nf_loc, front);
                         BFS_CHECK_LAUNCH();
                         ++launches;
                     }
-                    have_queue = false;
                 }
+                have_queue = false;
+                front_ok = false;
                 if (mg) {
                     g->comm->allgather_inplace(front, slice_bytes, s);
                     nvl = slice_bytes * (size_t)(p - 1);

@@ -56,6 +56,8 @@ struct Ctl {
     long long alpha, beta, n, arcs;
     int d, dir, have_queue, qsel, fsel, bu_done, returned, overflow;
     int mode, bu_from, max_levels, done;   // done: the persistent kernel's stop flag
+    long long claim_min;      // top-down steps with at least this many arcs run claim-only
+    int claim, front_ok;      // this step is claim-only; the front bitmap holds the frontier
 };
 // one record per step, filled by the step kernels (times: %globaltimer ns)
 struct LevelRec {

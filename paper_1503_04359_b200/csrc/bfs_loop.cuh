@@ -17,7 +17,7 @@
 __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip, int64_t pw,
                            int64_t root, const int32_t* __restrict__ label, int2* __restrict__ out, Queue q,
                            const int2* __restrict__ head, unsigned long long* __restrict__ cnt, Ctl* ctl,
-                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels) {
+                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels, int64_t claim_min) {
     const int64_t ri = label ? (int64_t)__ldg(label + root) : root;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
@@ -41,6 +41,7 @@ __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __res
         c.mode = pol.mode;
         c.bu_from = pol.bu_from_level;
         c.max_levels = max_levels;
+        c.claim_min = claim_min;
         *ctl = c;
     }
 }
@@ -83,10 +84,17 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
     if (c.dir == 0) {
         c.qsel ^= 1;
         c.have_queue = 1;
+        c.front_ok = 0;
+        if (c.claim) {            // the next frontier is also a bitmap (k_td_finish)
+            c.fsel ^= 1;
+            c.front_ok = 1;
+        }
     } else {
         c.fsel ^= 1;
         c.have_queue = 0;
+        c.front_ok = 0;
     }
+    c.claim = 0;
     c.prev_nf = c.n_f;
     c.n_f = next;
     c.m_f = c.m_fc = mf;
@@ -106,6 +114,7 @@ __global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, 
     const long long m_u = step_decide(c);
     c.E = c.m_f;
     c.nchunks = (c.E + kTdChunk - 1) / kTdChunk;
+    c.claim = c.dir == 0 && c.E >= c.claim_min;
     LevelRec r{};
     r.n_f = c.n_f;
     r.m_f = c.m_f;
@@ -129,15 +138,27 @@ __global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* c
 
 // top-down prologue: frontier bitmap -> queue when the previous step was bottom-up,
 // and a fresh tile state for the single-pass scan
-__global__ void k_td_prep(const Ctl* ctl, const uint32_t* __restrict__ f0, const uint32_t* __restrict__ f1,
+__global__ void k_td_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1,
                           int64_t words, const int2* __restrict__ head, Queue qa, Queue qb,
                           unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ tstate,
-                          unsigned int* __restrict__ tctr) {
+                          unsigned int* __restrict__ tctr, const uint32_t* __restrict__ visited) {
     const int64_t tiles = (ctl->n_f + 2047) / 2048;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tiles; i += (int64_t)gridDim.x * blockDim.x)
         tstate[i] = 0ull;
     if (blockIdx.x == 0 && threadIdx.x == 0) *tctr = 0u;
+    if (ctl->claim) {   // claim-only step: snapshot visited into the spare bitmap (k_td_finish)
+        uint32_t* snap = ctl->fsel ? f0 : f1;
+        for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
+            snap[w] = __ldcs(visited + w);
+    }
     if (!ctl->have_queue) b2q_body(ctl->fsel ? f1 : f0, words, 0, head, ctl->qsel ? qb : qa, cnt);
+}
+
+__global__ void k_td_finish_dev(const Ctl* ctl, const uint32_t* __restrict__ visited, uint32_t* __restrict__ f0,
+                                uint32_t* __restrict__ f1, int64_t words, const int2* __restrict__ head, Queue qa,
+                                Queue qb, unsigned long long* __restrict__ cnt) {
+    if (!ctl->claim) return;
+    td_finish_body(visited, ctl->fsel ? f0 : f1, words, head, ctl->qsel ? qa : qb, cnt);
 }
 
 // Single-pass exclusive scan of the current queue's degrees (decoupled look-back:
@@ -219,13 +240,13 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue
 
 // bottom-up prologue: queue -> bitmap when the previous step was top-down (clear, then set)
 __global__ void k_bu_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1, int64_t words) {
-    if (!ctl->have_queue) return;
+    if (!ctl->have_queue || ctl->front_ok) return;
     uint32_t* f = ctl->fsel ? f1 : f0;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
         f[w] = 0u;
 }
 __global__ void k_q2b_dev(const Ctl* ctl, Queue qa, Queue qb, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1) {
-    if (!ctl->have_queue) return;
+    if (!ctl->have_queue || ctl->front_ok) return;
     q2b_body((ctl->qsel ? qb : qa).v, ctl->n_f, ctl->fsel ? f1 : f0);
 }
 

@@ -66,7 +66,7 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
             const Queue qnext_in, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
-            int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec) {
+            int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec, int claim_only_in) {
     __shared__ int64_t s_pre[kTdStage + 2];
     __shared__ int64_t s_beg[kTdStage + 1];
     __shared__ int32_t s_u[kTdStage + 1];
@@ -85,6 +85,7 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         stamp_begin(lrec, ctl);
     }
     const Queue q = qc;
+    const bool claim_only = claim_only_in > 0 || (claim_only_in < 0 && ctl && ctl->claim);   // < 0: the loop state decides
     const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
     if (threadIdx.x == 0) s_qn = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -179,8 +180,17 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
             win[j] = false;
             if (wp[j] && !(wv[j] & bit)) win[j] = !(atomicOr(wp[j], bit) & bit);
         }
-        // C: outputs + staged queue append; remote claims go to the owner's list
+        // claim-only mode (large steps, see k_td_finish): winners record (depth, parent)
+        // -- only the claiming thread knows the parent -- but their degrees and the next
+        // queue are produced in vertex order by k_td_finish
+        if (claim_only) {
 #pragma unroll
+            for (int j = 0; j < kTdItems; ++j)
+                if (win[j]) __stcs(out + (v[j] - lo), make_int2(next_level, pmap ? __ldg(pmap + u[j]) : u[j]));
+            __syncthreads();
+            continue;
+        }
+        // C: outputs + staged queue append; remote claims go to the owner's list
         // winners' degrees (8-byte head records) and parent labels: all loads issued
         // before any is consumed, so their latencies overlap instead of adding up
         int32_t dgs[kTdItems], par[kTdItems];
@@ -236,6 +246,58 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         __syncthreads();
         stamp_end(lrec, ctl);
     }
+}
+
+// Second half of a large top-down step run in claim-only mode (single partition): the
+// winners are the bits the claims set (visited now, not in the snapshot taken before the
+// step), read back in vertex order, so their head-record reads (degree: m_f of the next
+// frontier) and queue appends are coalesced instead of scattered.  The snapshot becomes
+// the next frontier bitmap (a bottom-up step that follows needs no queue conversion).
+__device__ __forceinline__ void td_finish_body(const uint32_t* __restrict__ visited, uint32_t* __restrict__ snap,
+                                               int64_t words, const int2* __restrict__ head, const Queue qn,
+                                               unsigned long long* __restrict__ cnt) {
+    // warp per 32-word batch: one queue reservation (atomicAdd) per 1024 vertices
+    const int lane = threadIdx.x & 31;
+    unsigned long long my_mf = 0;
+    for (int64_t b0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; b0 < words;
+         b0 += (((int64_t)gridDim.x * blockDim.x) >> 5) * 32) {
+        const int64_t w = b0 + lane;
+        uint32_t nb = 0;
+        if (w < words) {
+            nb = __ldcg(visited + w) & ~__ldcg(snap + w);
+            snap[w] = nb;
+        }
+        const int c = __popc(nb);
+        int inc = c;
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, dd);
+            if (lane >= dd) inc += y;
+        }
+        const int tot = __shfl_sync(kFull, inc, 31);
+        if (!tot) continue;
+        unsigned long long base = 0;
+        if (lane == 0) base = atomicAdd(cnt + C_NEXT, (unsigned long long)tot);
+        base = __shfl_sync(kFull, base, 0);
+        const int excl = inc - c;
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t nk = __shfl_sync(kFull, nb, k);
+            if (!nk) continue;
+            const int ek = __shfl_sync(kFull, excl, k);
+            if ((nk >> lane) & 1u) {
+                const int64_t v = (b0 + k) * 32 + lane;
+                const int32_t dg = __ldg(head + v).y;
+                my_mf += (unsigned long long)dg;
+                queue_put(qn, base + ek + __popc(nk & lanemask_lt()), (int32_t)v, dg);
+            }
+        }
+    }
+    my_mf = warp_sum_u64(my_mf);
+    if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+}
+__global__ void k_td_finish(const uint32_t* __restrict__ visited, uint32_t* __restrict__ snap, int64_t words,
+                            const int2* __restrict__ head, const Queue qn, unsigned long long* __restrict__ cnt) {
+    td_finish_body(visited, snap, words, head, qn, cnt);
 }
 
 // Owner side of the top-down push: claims (v, parent) received from peers are

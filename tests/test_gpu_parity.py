@@ -345,3 +345,24 @@ def test_degenerate_and_ragged_graphs(loop, reindex):
             for pol in (dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=0)):
                 _check_outputs(g, ref, root, dict(loop=loop, **pol))
         g.close()
+
+
+@pytest.mark.parametrize("loop", ["graph", "host"])
+def test_claim_only_topdown_steps(loop, monkeypatch):
+    """Large top-down steps run claim-only + k_td_finish (winners read back in vertex order).
+    Forcing it on every top-down step (BFS_TD_CLAIM_MIN=1) must change nothing observable."""
+    monkeypatch.setenv("BFS_TD_CLAIM_MIN", "1")
+    for name in ("g1", "union", "skewed", "random", "grid"):
+        n, uv = FIXTURES[name]
+        g = pkg.Graph.from_edges(uv, n)
+        ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+        for root in sorted({0, n - 1, int(np.argmax(ref.degree()))}):
+            for pol in (dict(mode=0), dict(mode=1), dict(mode=3, alpha=500, beta=2)):
+                _check_run(g, ref, root, dict(loop=loop, **pol), uv)
+        g.close()
+    uv, ref = oracle.kron_graph(14, 16, 9)
+    g = pkg.Graph.kronecker(14, 16, 9, opts=pkg.default_opts(reindex_by_degree=True))
+    for r in g.sample_roots(14, 9, 4):
+        _check_outputs(g, ref, int(r), dict(loop=loop, mode=1))
+        _check_outputs(g, ref, int(r), dict(loop=loop, mode=0, alpha=30, beta=1000))
+    g.close()
