@@ -231,6 +231,33 @@ def test_host_output_buffers():
     g.close()
 
 
+@pytest.mark.parametrize("reindex", [False, True])
+@pytest.mark.parametrize("loop", ["host", "graph", "persistent"])
+def test_pinned_host_outputs(reindex, loop):
+    """pinned host outputs (the e2e leg of bench.py): every entry is overwritten
+    (buffers start as garbage), depth == oracle, parents valid, in every level loop
+    and with and without the degree reindex"""
+    scale = 14
+    g = pkg.Graph.kronecker(scale, 16, 9, opts=pkg.default_opts(reindex_by_degree=reindex))
+    g.set_policy(loop=loop)
+    uv, ref = oracle.kron_graph(scale, 16, 9)
+    n = 1 << scale
+    p = torch.full((n,), 0x5a5a5a5a, dtype=torch.int32).pin_memory()
+    d = torch.full((n,), 0x5a5a5a5a, dtype=torch.int32).pin_memory()
+    for r in g.sample_roots(scale, 9, 3):
+        p.fill_(0x5a5a5a5a)
+        d.fill_(0x5a5a5a5a)
+        pkg.bfs_run(g.h, int(r), p, d)
+        want, _ = oracle.bfs(ref, int(r))
+        assert np.array_equal(d.numpy(), want)
+        assert not oracle.validate(ref, int(r), d.numpy(), p.numpy(), ref_depth=want)
+        # depth only / parent only
+        d.fill_(0x5a5a5a5a)
+        pkg.bfs_run(g.h, int(r), None, d)
+        assert np.array_equal(d.numpy(), want)
+    g.close()
+
+
 def test_repeated_runs_and_stream():
     s = torch.cuda.Stream()
     scale = 14
