@@ -17,6 +17,8 @@ Functions and the passage each follows:
 * ``sort_rows_by_degree``     -- section 3.4 row order without relabeling
 * ``bfs``                     -- serial FIFO BFS, the plain definition
 * ``validate``                -- Graph500 validator V1-V6
+* ``stream_validate_edges`` / ``stream_validate_vertices`` -- the same rules V1-V5 over the
+  input tuples of R searches at once
 * ``do_emulate``              -- direction rule, counters, inspections
 * ``component_tuples``, ``compute_teps``, ``harmonic_mean`` -- TEPS (P:168; S:408-425)
 * ``sample_roots``            -- seeded root list (R8)
@@ -44,10 +46,11 @@ ER_ABC = (2500, 2500, 2500)    # all quadrants equal: uniform random multigraph
 
 
 def build_library(force: bool = False) -> str:
-    """Compile oracle.c with gcc (plain -O2, no OpenMP, no vectorisation hints)."""
+    """Compile oracle.c with gcc (-O3 for an x86-64-v3 (AVX2) host: integer code only, so the flags
+    cannot change a result; no OpenMP, no threads -- the harness runs ranges in parallel)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O3", "-march=x86-64-v3", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -74,6 +77,10 @@ def _L():
             lib.orc_bfs.restype = i64
             lib.orc_validate.argtypes = [i64, P, P, i64, P, P, P, P, P]
             lib.orc_validate.restype = i64
+            lib.orc_stream_validate_edges.argtypes = [i64, i32, P, i64, i64, P, P, P, P, P]
+            lib.orc_stream_validate_edges.restype = None
+            lib.orc_stream_validate_vertices.argtypes = [i64, i32, P, P, P, P, i64, i64, P, P]
+            lib.orc_stream_validate_vertices.restype = None
             lib.orc_do_emulate.argtypes = [i64, P, P, P, i64, i64, i32, i64, i64, P, P, P, P, P, P, P, i64]
             lib.orc_do_emulate.restype = i64
             lib.orc_component_tuples.argtypes = [i64, P, P]
@@ -217,6 +224,40 @@ def validate(g: CSR, root: int, depth, parent, ref_depth=None) -> dict:
     _L().orc_validate(g.n, _p(g.offsets), _p(adj), root, _p(d), _p(p), _p(r) if r is not None else None,
                       _p(fails), _p(first))
     return {RULES[i]: (int(fails[i]), int(first[i])) for i in range(6) if fails[i]}
+
+
+STREAM_RULES = ("V1_root", "V2_tree_edge", "V3_parent_depth", "V4_edge_span", "V5_unreached")
+
+
+def stream_validate_edges(n: int, uv, index0: int, depth8, parent, witness):
+    """Edge pass of the streaming validator over tuples uv (int32 [k, 2], tuple indices
+    index0..index0+k); depth8 int8 [n, R], parent int32 [n, R], witness uint8 [n, R]
+    (updated).  Returns (fails_v4 int64[R], first_v4 int64[R]).  Releases the GIL
+    (ctypes), so disjoint tuple ranges can be checked from several threads."""
+    R = depth8.shape[1]
+    assert depth8.dtype == np.int8 and parent.dtype == np.int32 and witness.dtype == np.uint8
+    assert depth8.shape == parent.shape == witness.shape == (n, R)
+    assert depth8.flags["C_CONTIGUOUS"] and parent.flags["C_CONTIGUOUS"] and witness.flags["C_CONTIGUOUS"]
+    uv = _c(uv, np.int32)
+    fails = np.zeros(R, np.int64)
+    first = np.full(R, -1, np.int64)
+    _L().orc_stream_validate_edges(n, R, _p(uv), uv.shape[0], index0, _p(depth8), _p(parent), _p(witness),
+                                   _p(fails), _p(first))
+    return fails, first
+
+
+def stream_validate_vertices(n: int, roots, depth8, parent, witness, v0: int = 0, v1: int | None = None):
+    """Vertex pass (V1, V2, V3, V5) over [v0, v1) after the edge pass saw every tuple.
+    Returns (fails int64[R, 5], first int64[R, 5]); column 3 (V4) stays 0."""
+    R = depth8.shape[1]
+    v1 = n if v1 is None else v1
+    rt = _c(roots, np.int64)
+    assert rt.shape == (R,)
+    fails = np.zeros((R, 5), np.int64)
+    first = np.full((R, 5), -1, np.int64)
+    _L().orc_stream_validate_vertices(n, R, _p(rt), _p(depth8), _p(parent), _p(witness), v0, v1, _p(fails),
+                                      _p(first))
+    return fails, first
 
 
 def do_emulate(g: CSR, depth, alpha: int = 15, beta: int = 18, policy: int = 0, bu_from: int = 0,

@@ -64,7 +64,7 @@ static void seed_key(uint64_t seed, uint32_t key[2]) {
 static uint32_t bitrev_s(uint32_t v, int scale) {
     uint32_t r = 0;
     for (int b = 0; b < scale; ++b)
-        if (v & (1u << b)) r |= 1u << (scale - 1 - b);
+        r |= ((v >> b) & 1u) << (scale - 1 - b);   /* bit b of v -> bit scale-1-b */
     return r;
 }
 
@@ -107,11 +107,12 @@ void orc_kron_edges(int scale, uint64_t seed, uint32_t a, uint32_t b, uint32_t c
             }
             uint32_t r = words[l % 4];
             uint32_t q = (uint32_t)(((uint64_t)r * 10000u) >> 32);
-            uint32_t row, col;
-            if (q < a)              { row = 0; col = 0; }
-            else if (q < a + b)     { row = 0; col = 1; }
-            else if (q < a + b + c) { row = 1; col = 0; }
-            else                    { row = 1; col = 1; }
+            /* the quadrant table above as comparisons (the same values, no data-
+             * dependent branch: a K29 pass regenerates 8.6 G tuples, section 8(c4)):
+             *   row = 1 iff q >= a+b             -- quadrants C, D
+             *   col = 1 iff a <= q < a+b  or  q >= a+b+c   -- quadrants B, D */
+            uint32_t row = (uint32_t)(q >= a + b);
+            uint32_t col = ((uint32_t)(q >= a) & (uint32_t)(q < a + b)) | (uint32_t)(q >= a + b + c);
             u |= row << l;
             v |= col << l;
         }
@@ -354,6 +355,81 @@ int64_t orc_validate(int64_t n, const int64_t* offsets, const int32_t* adj, int6
     int64_t total = 0;
     for (int r = 0; r < 6; ++r) total += fails[r];
     return total;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Streaming Graph500 validator (P:168
+ * "experimental methodology defined by Graph500").  The rules of orc_validate,
+ * checked against the input TUPLES themselves (regenerated by orc_kron_edges)
+ * instead of a CSR, for R searches of one graph at once, so it runs at scales
+ * where the serial oracle's CSR does not fit in host memory.
+ *
+ * Why it pins depths exactly (SURVEY c4 theorem): if V1-V5 hold then
+ *   - V2+V3+V1: following parents from a reached v walks real edges, one level
+ *     down per step, and can only stop at the root, so dist(v) <= depth(v);
+ *   - V4 along a shortest path r = x0, x1, ..., xk = v: depth(x_i) <= depth(x_{i-1}) + 1
+ *     and every x_i is reached, so depth(v) <= k = dist(v);
+ *   - V4 carries reachability across every edge, and V5 makes the unreached
+ *     exactly the vertices with depth -1: the reached set is the root's component.
+ * Hence depth == the hop distance == the serial oracle's depth, vertex by vertex.
+ *
+ * Layout (vertex-major so one tuple touches one cache line per endpoint per array):
+ *   depth8[v * R + r]   int8  depth of v in search r, -1 unreached (callers check depth < 127)
+ *   parent[v * R + r]   int32 parent of v in search r, -1 unreached
+ *   witness[v * R + r]  uint8 set to 1 by the edge pass when a tuple {parent[v], v} exists
+ *
+ * Edge pass over tuples uv[0..count) (tuple indices index0...): for every tuple
+ * {a, b} and search r
+ *   V4: both reached with |depth a - depth b| <= 1, or both unreached;
+ *   V2 witness: parent[b] == a  =>  witness[b] = 1;  parent[a] == b  =>  witness[a] = 1.
+ * fails_v4[r] counts failing tuples, first_v4[r] = index of the first one (or -1).
+ * Passes over disjoint tuple ranges may run concurrently: witness bytes only ever
+ * go 0 -> 1 (atomic store). */
+void orc_stream_validate_edges(int64_t n, int R, const int32_t* uv, int64_t count, int64_t index0,
+                               const int8_t* depth8, const int32_t* parent, uint8_t* witness,
+                               int64_t* fails_v4, int64_t* first_v4) {
+    for (int64_t k = 0; k < count; ++k) {
+        int64_t a = uv[2 * k], b = uv[2 * k + 1];
+        if (a < 0 || a >= n || b < 0 || b >= n) continue;   /* not a tuple of this graph */
+        for (int r = 0; r < R; ++r) {
+            int da = depth8[a * R + r], db = depth8[b * R + r];
+            int ra = da >= 0, rb = db >= 0;
+            if (ra != rb || (ra && (da - db > 1 || db - da > 1))) {
+                if (fails_v4[r]++ == 0) first_v4[r] = index0 + k;
+            }
+            if (parent[b * R + r] == (int32_t)a) __atomic_store_n(&witness[b * R + r], (uint8_t)1, __ATOMIC_RELAXED);
+            if (parent[a * R + r] == (int32_t)b) __atomic_store_n(&witness[a * R + r], (uint8_t)1, __ATOMIC_RELAXED);
+        }
+    }
+}
+
+/* Vertex pass over v in [v0, v1), after every tuple went through the edge pass;
+ * the per-vertex rules in orc_validate's order:
+ *   V1 root: parent = root and depth 0; depth 0 only at the root
+ *   V5 reached (depth >= 0) <=> parent >= 0; depth, parent >= -1; parent < n
+ *   V2 every reached v != root has its witness (the tuple {parent[v], v} exists)
+ *   V3 depth[parent[v]] = depth[v] - 1 for every reached v != root
+ * fails[r * 5 + i] counts failures of rule V(i+1) (slot 3 = V4 belongs to the
+ * edge pass and stays 0), first[r * 5 + i] the first offending vertex (or -1). */
+void orc_stream_validate_vertices(int64_t n, int R, const int64_t* roots, const int8_t* depth8,
+                                  const int32_t* parent, const uint8_t* witness, int64_t v0, int64_t v1,
+                                  int64_t* fails, int64_t* first) {
+#define SFAIL(r, i, v) do { if (fails[(r) * 5 + (i)]++ == 0) first[(r) * 5 + (i)] = (v); } while (0)
+    for (int64_t v = v0; v < v1; ++v) {
+        for (int r = 0; r < R; ++r) {
+            int d = depth8[v * R + r];
+            int32_t p = parent[v * R + r];
+            int64_t root = roots[r];
+            if (v == root && (p != (int32_t)root || d != 0)) SFAIL(r, 0, v);
+            if ((d >= 0) != (p >= 0) || d < -1 || p < -1 || p >= n) { SFAIL(r, 4, v); continue; }
+            if (d < 0) continue;
+            if (d == 0 && v != root) SFAIL(r, 0, v);
+            if (v == root) continue;
+            if (!witness[v * R + r]) SFAIL(r, 1, v);
+            if (depth8[(int64_t)p * R + r] != d - 1) SFAIL(r, 2, v);
+        }
+    }
+#undef SFAIL
 }
 
 /* ------------------------------------------------------------------------- */

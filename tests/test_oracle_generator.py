@@ -128,3 +128,37 @@ def test_uniform_special_case_chi_square():
         chi2 = float(((cnt - e) ** 2 / e).sum())
         dof = (1 << s) - 1
         assert abs(chi2 - dof) < 5 * math.sqrt(2 * dof), chi2
+
+
+def _rank(x):
+    r = np.empty(len(x))
+    r[np.argsort(x, kind="stable")] = np.arange(len(x))
+    return r
+
+
+@pytest.mark.parametrize("seed", [1, 2, 7])
+def test_scramble_randomly_permutes_labels(seed):
+    """S:104 "vertex labels are randomly permuted after generation": besides being a
+    bijection (above) the scramble must look like a random permutation.  A uniform
+    random permutation of n labels has Poisson(1) fixed points and a Spearman rank
+    correlation with the identity of sd 1/sqrt(n-1); the pre-scramble popcount (which
+    fixes a vertex's expected degree, SURVEY c1 v') must not predict the new label.
+    An identity or order-preserving "scramble" fails every one of these."""
+    s = 16
+    n = 1 << s
+    keys = oracle.scramble_keys(seed)
+    v = np.arange(n)
+    img = np.array([oracle.scramble(s, keys, int(x)) for x in v], np.int64)
+    assert img[0] != 0
+    assert int((img == v).sum()) <= 8                      # P(Poisson(1) > 8) < 1e-6
+    sd = 1 / math.sqrt(n - 1)
+    rho = np.corrcoef(_rank(v), _rank(img))[0, 1]
+    assert abs(rho) < 5 * sd, rho
+    pop = np.array([bin(x).count("1") for x in range(n)], np.float64)
+    r_pop = np.corrcoef(pop, img.astype(np.float64))[0, 1]
+    assert abs(r_pop) < 5 * sd, r_pop
+    # the 17 highest-expected-degree labels (popcount <= 1) land anywhere: their mean
+    # new label is within 5 sd of (n-1)/2 (sd of a mean of k uniform draws)
+    top = img[pop <= 1].astype(np.float64)
+    assert abs(top.mean() - (n - 1) / 2) < 5 * (n / math.sqrt(12 * len(top))), top.mean()
+
