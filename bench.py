@@ -45,8 +45,9 @@ PAPER_GTEPS = {"k29": 17.3}
 ROOTS = 64
 # random 4-byte L2 probes per second on B200 (measured: profiles/r01_l2_probe_micro.txt)
 L2_PROBE_PEAK = 270.0
-# cpu_baseline / reference arm sample: the oracle cannot build s26+ within the bench budget
-SAMPLE_SCALE = 20
+# cpu_baseline / reference arm: the largest Kronecker scale whose oracle graph builds
+# within the bench budget (~1 min of host time on the GPU boxes)
+CPU_SCALE = 24
 
 
 def measured_peaks():
@@ -125,30 +126,78 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- oracle legs
-def oracle_sample(budget_s: float, roots_max: int = ROOTS, seed: int = 1):
-    """Serial oracle BFS on the bounded sample graph: list of (gteps, seconds) per root."""
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_threads() -> int:
+    return max(1, min(ROOTS, os.cpu_count() or 1))
+
+
+def oracle_setup(scale: int, seed: int, abc, nroots: int = ROOTS):
+    """The serial oracle's own graph (oracle.kron_edges tuples -> oracle.build_csr, the
+    same options as the GPU build) and root sample.  Tuples are generated over
+    disjoint index ranges on host threads (harness parallelism: each range is the
+    unmodified serial generator); the CSR build is the oracle's, single-threaded."""
+    import concurrent.futures as cf
+
+    import numpy as np
+
     import oracle
-    uv, g = oracle.kron_graph(SAMPLE_SCALE, 16, seed)
-    roots = oracle.sample_roots(g, SAMPLE_SCALE, seed, roots_max)
-    out = []
-    t_all = time.perf_counter()
-    for r in roots:
+    m = 16 << scale
+    uv = np.empty((m, 2), np.int32)
+    step = 1 << 22
+
+    def gen(lo):
+        uv[lo:lo + step] = oracle.kron_edges(scale, 16, seed, abc, first=lo, count=min(step, m - lo))
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(oracle_threads()) as ex:
+        list(ex.map(gen, range(0, m, step)))
+    g = oracle.build_csr(1 << scale, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    roots = oracle.sample_roots(g, scale, seed, nroots)
+    return uv, g, roots, time.perf_counter() - t0
+
+
+def oracle_batch(uv, g, roots, threads: int):
+    """One serial oracle BFS per root, `threads` roots at a time on the host cores
+    (every search itself is serial and timed alone): [(gteps, seconds), ...]."""
+    import concurrent.futures as cf
+
+    import oracle
+
+    def one(r):
         t0 = time.perf_counter()
         depth, _ = oracle.bfs(g, int(r))
         dt = time.perf_counter() - t0
-        e = oracle.component_tuples(uv, depth)
-        out.append((e / dt / 1e9, dt))
-        if time.perf_counter() - t_all > budget_s:
-            break
-    return out, (uv, g, roots)
+        return oracle.component_tuples(uv, depth) / dt / 1e9, dt
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        return list(ex.map(one, roots))
 
 
-def cpu_baseline_record(budget_s: float = 15.0):
-    res, _ = oracle_sample(budget_s)
-    return {"value": round(hmean(r for r, _ in res), 6), "unit": "GTEPS", "cores": 1, "kind": "oracle",
-            "sample": f"serial FIFO oracle (oracle/oracle.c, 1 thread) on Graph500 Kronecker s{SAMPLE_SCALE} ef16 "
-                      f"seed 1, {len(res)} roots, harmonic mean; the oracle cannot build the s26+ CSR within the "
-                      f"bench budget (s29 needs 68 GiB host RAM and ~1 h of single-core generation)"}
+def oracle_sample_text(scale: int, nroots: int, threads: int, build_s: float) -> str:
+    return (f"serial FIFO oracle (oracle/oracle.c orc_bfs) on Graph500 Kronecker s{scale} ef16 seed 1 "
+            f"(dedup, self-loops dropped), {nroots} sampled roots, {threads} roots at a time on "
+            f"{threads} host threads (each search serial on one thread, timed on it while the others run; "
+            f"GTEPS per search, harmonic mean); "
+            f"host: {os.cpu_count()} cores, {cpu_model()}; oracle graph build {build_s:.0f} s untimed. "
+            f"The benched scale needs ~73 GB and ~1 h of single-threaded oracle CSR build: out of the bench budget")
+
+
+def cpu_baseline_record(scale: int):
+    uv, g, roots, build_s = oracle_setup(scale, 1, KRON)
+    th = oracle_threads()
+    res = oracle_batch(uv, g, roots, th)
+    return {"value": round(hmean(r for r, _ in res), 6), "unit": "GTEPS", "cores": th, "kind": "oracle",
+            "sample": oracle_sample_text(scale, len(roots), th, build_s), "scale": scale}
 
 
 def run_reference(args):
@@ -156,47 +205,41 @@ def run_reference(args):
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
-    import oracle
-    t0 = time.perf_counter()
-    uv, g = oracle.kron_graph(SAMPLE_SCALE, 16, 1)
-    build_s = time.perf_counter() - t0
-    roots = oracle.sample_roots(g, SAMPLE_SCALE, 1, ROOTS)
-    per_step = max(1, min(ROOTS, int(150.0 / max(1, args.steps + args.warmup) / 0.35)))
+    scale = min(cfg["scale"], args.cpu_scale)
+    uv, g, roots, build_s = oracle_setup(scale, cfg["seed"], cfg["abc"])
+    th = oracle_threads()
     rates, step_ms = [], []
-    ri = 0
     for step in range(args.warmup + args.steps):
-        t_step = 0.0
-        for _ in range(per_step):
-            r = int(roots[ri % len(roots)])
-            ri += 1
-            t1 = time.perf_counter()
-            depth, _ = oracle.bfs(g, r)
-            dt = time.perf_counter() - t1
-            t_step += dt
-            if step >= args.warmup:
-                rates.append(oracle.component_tuples(uv, depth) / dt / 1e9)
+        t0 = time.perf_counter()
+        res = oracle_batch(uv, g, roots, th)
         if step >= args.warmup:
-            step_ms.append(t_step * 1e3)
+            step_ms.append((time.perf_counter() - t0) * 1e3)
+            rates += [r for r, _ in res]
     v = hmean(rates)
-    sample = (f"serial FIFO oracle (1 thread) on Graph500 Kronecker s{SAMPLE_SCALE} ef16 seed 1 ({per_step} roots "
-              f"per step, oracle CSR build {build_s:.1f} s untimed); the {cfg['name']} CSR is out of reach of the "
-              f"serial oracle within the bench budget")
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": "GTEPS", "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 3),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
-            "data": "synthetic", "config": {"workload": cfg["name"], "sample_scale": SAMPLE_SCALE,
-                                            "roots_per_step": per_step},
-            "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": 1, "kind": "oracle", "sample": sample},
+            "data": "synthetic", "config": {"workload": cfg["name"], "sample_scale": scale, "roots_per_step": len(roots)},
+            "cpu_baseline": {"value": round(v, 6), "unit": "GTEPS", "cores": th, "kind": "oracle",
+                             "sample": oracle_sample_text(scale, len(roots), th, build_s)},
             "e2e": {"value": round(v, 6), "unit": "GTEPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- our arm
-def bu_bytes(n_global: int, lv: dict) -> int:
-    """Algorithmic bytes of one bottom-up launch: visited scan,
-    frontier and next bitmaps (3 n/8), offsets of scanned vertices (8 U), arcs
-    inspected (4 insp), outputs of discovered vertices (8 D)."""
-    return 3 * n_global // 8 + 8 * lv["scanned"] + 4 * lv["inspections"] + 8 * lv["discovered"]
+def bu_bytes(n_bits: int, lv: dict) -> int:
+    """Algorithmic bytes of one bottom-up launch, SURVEY section 8(d) exactly: visited
+    scan, frontier and next bitmaps over the n_bits vertices the step covers (3 n/8;
+    the non-isolated prefix when reindexed on one GPU), offsets of the U scanned
+    vertices (8 U), arcs inspected (4 insp).  Outputs are charged once per search
+    (8 n), not per launch."""
+    return 3 * n_bits // 8 + 8 * lv["scanned"] + 4 * lv["inspections"]
+
+
+def bu_design_bytes(lv: dict) -> int:
+    """This design's extra per-launch bytes: the (depth, parent) record of every
+    discovered vertex (8 D), re-read by the output pass."""
+    return 8 * lv["discovered"]
 
 
 def td_bytes(lv: dict) -> int:
@@ -227,6 +270,10 @@ def main():
     ap.add_argument("--rows", default="id", choices=["id", "degree"],
                     help="row order: ascending ID (sort_rows 1) or decreasing neighbour degree (2, P:158)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-scale", type=int, default=CPU_SCALE,
+                    help="Kronecker scale of the oracle's sample (cpu_baseline and --impl reference)")
+    ap.add_argument("--no-validate", action="store_true",
+                    help="skip the Graph500 validation (bfs_validate) of the last timed step's searches")
     ap.add_argument("--levels-out", default=None, help="write per-level records (JSON) here")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -275,34 +322,50 @@ def main():
     else:
         g.set_policy(mode=0, alpha=args.alpha, beta=args.beta, level_times=True)
 
+    pkg._check_output(parent, nl, "parent")   # the buffers are checked once, not per timed call
+    pkg._check_output(depth, nl, "depth")
+
     def one(r):
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        pkg.bfs_run(g.h, int(r), parent, depth)
+        pkg.bfs_run(g.h, int(r), parent, depth, check=False)
         ev1.record(stream)
         ev1.synchronize()
         return ev0.elapsed_time(ev1)
 
-    # warm-up: also caches the TEPS numerator per root (outside the timed region)
+    # TEPS numerator of every root: one untimed search each (independent of --warmup)
     edges = {}
+    for r in roots:
+        one(r)
+        edges[int(r)] = pkg.bfs_component_tuples(g.h)
     for _ in range(args.warmup):
         for r in roots:
             one(r)
-            if int(r) not in edges:
-                edges[int(r)] = pkg.bfs_component_tuples(g.h)
 
     times, launches = [], 0
     kern = {"bu": [0.0, 0, 0], "td": [0.0, 0, 0]}   # ms, bytes, launches
     probes = {"bu": 0, "td": 0}                      # frontier / visited probes (= inspections)
     levels_dump = []
     nvl_level_bytes = []
+    design_bytes = 0
+    n_bits = pkg.bfs_graph_active(g.h)
+    # Graph500 validation of every search of the last timed step, after its
+    # events completed (outside the timed region): bfs_validate on the device
+    do_val = not args.no_validate and ws == 1
+    val = {"searches": 0, "failed_searches": 0, "rules": {}}
     barrier()
     with ClockSampler(local) as clk:
         for step in range(args.steps):
             for r in roots:
                 ms = one(r)
                 run, levels = g.stats(tuples=False)
+                if do_val and step == args.steps - 1:
+                    bad = pkg.bfs_validate(g.h, int(r), parent, depth)
+                    val["searches"] += 1
+                    val["failed_searches"] += bool(bad)
+                    for k, v in bad.items():
+                        val["rules"][k] = val["rules"].get(k, 0) + v
                 times.append(ms)
                 launches += run["kernel_launches"]
                 nvl_level_bytes += [lv["nvlink_bytes"] for lv in levels]
@@ -311,7 +374,8 @@ def main():
                     if key == "td" and lv["m_f"] == 0:
                         continue
                     kern[key][0] += lv["kernel_ms"]
-                    kern[key][1] += bu_bytes(n, lv) if key == "bu" else td_bytes(lv)
+                    kern[key][1] += bu_bytes(n_bits, lv) if key == "bu" else td_bytes(lv)
+                    design_bytes += bu_design_bytes(lv) if key == "bu" else 0
                     kern[key][2] += 1
                     probes[key] += lv["inspections"]
                 if step == 0:
@@ -331,11 +395,13 @@ def main():
     kms, kbytes, klaunch = kern[dom]
     peak, peak_kind = measured_peaks()
     achieved = (kbytes / klaunch) / ((kms / klaunch) * 1e-3) / 1e9 if klaunch and kms > 0 else 0.0
-    traffic = None
+    traffic, traffic_src = None, None
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get("k_bu_batch" if dom == "bu" else "k_td_expand")
+            tj = json.load(f)
+        traffic = tj.get("k_bu_batch" if dom == "bu" else "k_td_expand")
+        traffic_src = tj.get("source")
     total_ms = sum(times)
     share = kms / total_ms if total_ms else 0.0
 
@@ -366,7 +432,7 @@ def main():
         with open(args.levels_out, "w") as f:
             json.dump(levels_dump, f)
 
-    cpu = None if (args.no_cpu_baseline or ws > 1) else cpu_baseline_record()
+    cpu = None if (args.no_cpu_baseline or ws > 1) else cpu_baseline_record(min(cfg["scale"], args.cpu_scale))
     line = {
         "metric": METRIC, "value": round(value, 4), "unit": "GTEPS", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(statistics.mean(step_ms), 4), "higher_is_better": True,
@@ -385,9 +451,16 @@ def main():
         "gteps_min_median_max": [round(min(rates), 3), round(statistics.median(rates), 3), round(max(rates), 3)],
         "roofline": {"bound": "hbm", "kernel": "k_bu_batch" if dom == "bu" else "k_td_expand",
                      "achieved": round(achieved, 2), "peak": peak, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_kind": peak_kind,
-                     "share_of_step": round(share, 4), "launches": klaunch,
-                     "bytes_per_launch": int(kbytes / klaunch) if klaunch else 0},
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "traffic_source": traffic_src,
+                     "peak_kind": peak_kind, "share_of_step": round(share, 4), "launches": klaunch,
+                     "bytes_per_launch": int(kbytes / klaunch) if klaunch else 0,
+                     "ms_per_launch": round(kms / klaunch, 5) if klaunch else None,
+                     "bytes_model": ("BU: 3*n_bits/8 + 8*scanned + 4*inspections per launch (SURVEY 8(d)); "
+                                     "TD: 20*F + 4*m_f + 20*D" if dom == "bu" else "TD: 20*F + 4*m_f + 20*D"),
+                     "n_bits": n_bits,
+                     "design_bytes_per_launch": int(design_bytes / klaunch) if (klaunch and dom == "bu") else None,
+                     "timing": "per launch: %globaltimer span inside the kernel (first block start to last block "
+                               "end), summed over the timed region's launches"},
         # second roofline for the probe-bound levels: every inspection is one random
         # 4-byte bitmap probe; B200 serves <= ~270 G such probes/s from L2
         # (profiles/r01_l2_probe_micro.txt, tools/micro/l2probe.cu)
@@ -400,6 +473,8 @@ def main():
             "bytes_per_bfs_mean": sum(nvl_level_bytes) / max(1, len(times)),
             "link_gbs_ref": 900.0, "note": "bytes this rank sent to peers (rank 0)"},
         "clocks": clocks,
+        "validation": (dict(val, note="bfs_validate (Graph500 V1-V5 on the device) on every search of the last "
+                                      "timed step") if do_val else None),
         "e2e": e2e,
         "cpu_baseline": cpu,
     }

@@ -168,6 +168,12 @@ bfs_status bfs_graph_create_csr(const int64_t* offsets, const int32_t* adj, int6
  * reindexed; the outputs of bfs_run are in original labels either way). */
 bfs_status bfs_graph_info(bfs_graph_t g, int64_t* n, int64_t* arcs, int64_t* local_begin, int64_t* local_end);
 
+/* Vertices the per-search bitmaps and bottom-up scans cover on this rank: with the
+ * degree reindex on one GPU the non-isolated prefix [0, n_active) of the internal
+ * labels (isolated vertices sit at the tail and never change state), else the
+ * owned range.  Lets measurements charge bitmap bytes per launch exactly. */
+bfs_status bfs_graph_active(bfs_graph_t g, int64_t* n_active);
+
 /* Construction time of the last bfs_graph_create on this handle (device ms). */
 bfs_status bfs_graph_build_ms(bfs_graph_t g, double* ms);
 
@@ -197,6 +203,18 @@ bfs_status bfs_stats(bfs_graph_t g, bfs_run_stats* out, bfs_level_stats* levels,
  * (R5) = sum of raw degrees over reached vertices / 2, reduced on
  * the device (collective on p ranks).  Meant to be called outside timed regions. */
 bfs_status bfs_component_tuples(bfs_graph_t g, int64_t* tuples);
+
+/* Graph500 validation of a search's outputs on the device: the
+ * benchmark's self-check, run outside timed regions.  parent/depth: the n-entry
+ * outputs of bfs_run for `root` (original labels; host or device).  fails[0..5)
+ * receive the number of violations of V1 (root: parent = root, depth 0; depth 0
+ * only at the root), V2 (tree edge {parent[v], v} is a stored arc), V3
+ * (depth[parent[v]] = depth[v] - 1), V4 (no stored arc joins reached and unreached
+ * vertices or spans more than one level) and V5 (unreached <=> parent = depth = -1;
+ * parent < n).  All zero = a valid BFS tree with exact depths (the theorem in
+ * oracle/oracle.c).  Returns BFS_OK whether or not the outputs are valid; errors
+ * only for bad arguments (BFS_ERR_INVALID_ARG on a multi-partition graph). */
+bfs_status bfs_validate(bfs_graph_t g, int64_t root, const int32_t* parent, const int32_t* depth, int64_t fails[5]);
 
 bfs_status bfs_graph_destroy(bfs_graph_t g);
 

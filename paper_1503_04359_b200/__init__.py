@@ -32,7 +32,8 @@ EXPORTS = ("bfs_graph_create", "bfs_graph_create_kronecker", "bfs_graph_create_e
            "bfs_graph_info", "bfs_graph_build_ms", "bfs_set_policy", "bfs_run", "bfs_stats", "bfs_graph_destroy",
            "bfs_comm_unique_id", "bfs_comm_create", "bfs_comm_create_local", "bfs_comm_destroy", "bfs_last_error",
            "bfs_kronecker_edges", "bfs_graph_export_csr", "bfs_graph_export_labels", "bfs_sample_roots",
-           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row", "bfs_component_tuples")
+           "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row", "bfs_component_tuples",
+           "bfs_validate", "bfs_graph_active")
 
 
 class BfsError(RuntimeError):
@@ -112,6 +113,8 @@ def lib() -> ctypes.CDLL:
             "bfs_partition_range": [i64, i32, i32, P, P],
             "bfs_graph_export_row": [P, i64, P, i64, P],
             "bfs_component_tuples": [P, P],
+            "bfs_validate": [P, i64, P, P, P],
+            "bfs_graph_active": [P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -187,6 +190,13 @@ def bfs_graph_info(h):
     return tuple(x.value for x in v)
 
 
+def bfs_graph_active(h) -> int:
+    """Vertices the per-search bitmaps cover (non-isolated prefix when reindexed on one GPU)."""
+    x = ctypes.c_int64()
+    _check(lib().bfs_graph_active(h, ctypes.byref(x)))
+    return x.value
+
+
 def bfs_graph_build_ms(h) -> float:
     x = ctypes.c_double()
     _check(lib().bfs_graph_build_ms(h, ctypes.byref(x)))
@@ -204,7 +214,35 @@ def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_le
     _check(lib().bfs_set_policy(h, ctypes.byref(p)))
 
 
-def bfs_run(h, root: int, parent_out, depth_out):
+def _check_output(x, nl: int, name: str):
+    """An output buffer must be int32, contiguous and hold the nl owned vertices, in
+    device memory of the current device or in (pinned or pageable) host memory."""
+    if x is None:
+        return
+    if hasattr(x, "data_ptr"):       # torch tensor
+        import torch
+        if x.dtype != torch.int32:
+            raise ValueError(f"{name}: dtype {x.dtype}, expected torch.int32")
+        if not x.is_contiguous():
+            raise ValueError(f"{name}: not contiguous")
+        if x.numel() < nl:
+            raise ValueError(f"{name}: {x.numel()} elements < {nl} owned vertices")
+        if x.is_cuda and x.device.index != torch.cuda.current_device():
+            raise ValueError(f"{name}: on {x.device}, the graph's device is cuda:{torch.cuda.current_device()}")
+    elif isinstance(x, np.ndarray):
+        if x.dtype != np.int32 or not x.flags["C_CONTIGUOUS"] or x.size < nl:
+            raise ValueError(f"{name}: needs a contiguous int32 array of >= {nl} elements")
+    else:
+        raise ValueError(f"{name}: expected a torch tensor or numpy array, got {type(x).__name__}")
+
+
+def bfs_run(h, root: int, parent_out, depth_out, check: bool = True):
+    """parent_out / depth_out: int32 buffers of local_end - local_begin entries (device or host).
+    check=False skips the buffer checks (timed loops that checked the same buffers once)."""
+    if check:
+        _, _, lo, hi = bfs_graph_info(h)
+        _check_output(parent_out, hi - lo, "parent_out")
+        _check_output(depth_out, hi - lo, "depth_out")
     _check(lib().bfs_run(h, int(root), _ptr(parent_out), _ptr(depth_out)))
 
 
@@ -225,6 +263,17 @@ def bfs_stats(h, max_levels: int | None = None):
     levels = [{f: getattr(lv[i], f) for f, _ in bfs_level_stats._fields_} for i in range(min(rs.levels, max_levels))]
     run = {f: getattr(rs, f) for f, _ in bfs_run_stats._fields_}
     return run, levels
+
+
+VALIDATE_RULES = ("V1_root", "V2_tree_edge", "V3_parent_depth", "V4_edge_span", "V5_unreached")
+
+
+def bfs_validate(h, root: int, parent, depth) -> dict:
+    """Graph500 validation of one search's outputs on the device (S:362-370);
+    {rule: violations} for failing rules only ({} = valid)."""
+    f = np.zeros(5, np.int64)
+    _check(lib().bfs_validate(h, int(root), _ptr(parent), _ptr(depth), _ptr(f)))
+    return {VALIDATE_RULES[i]: int(f[i]) for i in range(5) if f[i]}
 
 
 def bfs_graph_destroy(h):

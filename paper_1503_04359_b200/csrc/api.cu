@@ -273,6 +273,14 @@ bfs_status bfs_graph_info(bfs_graph_t g, int64_t* n, int64_t* arcs, int64_t* loc
     API_END
 }
 
+bfs_status bfs_graph_active(bfs_graph_t g, int64_t* n_active) {
+    API_BEGIN
+    if (!g || !n_active) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    const bool active = g->reindexed && !(g->comm && g->comm->nranks > 1) && g->nparts == 1;
+    *n_active = active ? g->n_active : g->nl();
+    API_END
+}
+
 bfs_status bfs_graph_build_ms(bfs_graph_t g, double* ms) {
     API_BEGIN
     if (!g || !ms) fail(BFS_ERR_INVALID_ARG, "NULL argument");
@@ -319,6 +327,14 @@ bfs_status bfs_component_tuples(bfs_graph_t g, int64_t* tuples) {
     BFS_CUDA(cudaSetDevice(g->device));
     if (g->run.component_edge_tuples < 0) g->run.component_edge_tuples = component_tuples_impl(g);
     *tuples = g->run.component_edge_tuples;
+    API_END
+}
+
+bfs_status bfs_validate(bfs_graph_t g, int64_t root, const int32_t* parent, const int32_t* depth, int64_t fails[5]) {
+    API_BEGIN
+    if (!g || !fails) fail(BFS_ERR_INVALID_ARG, "NULL argument");
+    BFS_CUDA(cudaSetDevice(g->device));
+    validate_impl(g, root, parent, depth, fails);
     API_END
 }
 

@@ -180,8 +180,9 @@ static void sync_counters(bfs_graph_s* g) {
 template <class T>
 static void ensure(DevBuf<T>& b, size_t count, cudaStream_t s) {
     if (b.count < count) {
+        const size_t want = std::max(count, b.count * 2);   // geometric growth: few reallocations
         b.reset();
-        b.alloc(std::max(count, b.count * 2), s);
+        b.alloc(want, s);
     }
 }
 
@@ -300,8 +301,11 @@ static int pers_blocks_per_sm() {
     return e ? std::max(1, atoi(e)) : 1;
 }
 
-// co-resident CTAs of the persistent kernel (cooperative launch limit)
+// co-resident CTAs of the persistent kernel (cooperative launch limit).
+// BFS_PERSIST_GRID overrides it (tests: a grid too large to be co-resident must make
+// the cooperative launch fail and the search run as the loop graph instead).
 static int pers_grid() {
+    if (const char* e = getenv("BFS_PERSIST_GRID")) return std::max(1, atoi(e));
     static const int gsz = [] {
         int per = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bfs_persistent, kPersThreads, 0) != cudaSuccess ||
@@ -323,22 +327,26 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
     if (persistent) {
-        if (!g->ctl.p) build_loop_graph(g);   // the state buffers (the graph itself stays unused)
+        if (!g->ctl.p) {   // the state buffers (the graph itself is the fallback)
+            build_loop_graph(g);
+            g->loop_key = {bu_long_setting(), bu_dense_setting()};
+        }
         if (!g->big.p) g->big.alloc((size_t)(g->arcs_local / kPersBig + 4), s);   // + 2 barrier words
     }
     // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
     const std::vector<int> key{bu_long_setting(), bu_dense_setting()};
-    if (!persistent && g->loop_exec && g->loop_key != key) {
-        BFS_CUDA(cudaStreamSynchronize(s));
-        cudaGraphExecDestroy(g->loop_exec);
-        cudaGraphDestroy(g->loop_graph);
-        g->loop_exec = nullptr;
-        g->loop_graph = nullptr;
-    }
-    if (!persistent && !g->loop_exec) {
-        build_loop_graph(g);
+    auto ensure_loop_graph = [&] {
+        if (g->loop_exec && g->loop_key != key) {
+            BFS_CUDA(cudaStreamSynchronize(s));
+            cudaGraphExecDestroy(g->loop_exec);
+            cudaGraphDestroy(g->loop_graph);
+            g->loop_exec = nullptr;
+            g->loop_graph = nullptr;
+        }
+        if (!g->loop_exec) build_loop_graph(g);
         g->loop_key = key;
-    }
+    };
+    if (!persistent) ensure_loop_graph();
     Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
     const Queue qa{g->q0.p, g->qd0.p};
     const int64_t pw = reset_words(g);
@@ -363,11 +371,33 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         if (!g->pcnt.p) g->pcnt.alloc(48, s);
         BFS_CUDA(cudaMemsetAsync(g->pcnt.p, 0, 48 * sizeof(int64_t), s));
         BFS_CUDA(cudaMemcpyAsync(g->pcnt.p, cntp, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
-        k_bfs_persistent<<<pers_grid(), kPersThreads, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, g->front.p,
-                                                              g->next.p, words, g->rec.p, pmap, hpar, qa, qb,
-                                                              (unsigned long long*)g->pcnt.p, g->big.p, ctl, lrec,
-                                                              GridBar{bar, bar + 1});
-        BFS_CHECK_LAUNCH();
+        // the grid barrier needs every CTA resident at once: a cooperative launch
+        // guarantees it or fails (instead of hanging when other work holds SMs)
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(pers_grid());
+        cfg.blockDim = dim3(kPersThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_bfs_persistent, (const int64_t*)g->off.p,
+                                                 (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p,
+                                                 g->front.p, g->next.p, words, g->rec.p, pmap, hpar, qa, qb,
+                                                 (unsigned long long*)g->pcnt.p, g->big.p, ctl, lrec,
+                                                 GridBar{bar, bar + 1});
+        if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources) {
+            // the persistent grid cannot be co-resident now: the loop graph runs the
+            // same steps from the state k_init_dev wrote
+            cudaGetLastError();
+            persistent = false;
+            ensure_loop_graph();
+            BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
+            ++g->coop_fallbacks;
+        } else {
+            BFS_CUDA(e);
+        }
     } else {
         BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
     }

@@ -176,6 +176,7 @@ struct bfs_graph_s {
     bfs_policy policy{0, 15, 18, 0, 0, 0};
     bfsb::DevBuf<int32_t> big;       // persistent kernel: big frontier rows of a top-down step
     bfsb::DevBuf<int64_t> pcnt;      // persistent kernel: three counter sets
+    int64_t coop_fallbacks = 0;      // persistent searches that ran as the loop graph (grid not co-resident)
     std::vector<bfs_level_stats> levels;
     bfs_run_stats run{};
     int64_t last_root_l = 0;
@@ -198,6 +199,8 @@ void bfs_alloc_state(bfs_graph_s* g);
 void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out);
 void bfs_release_loop(bfs_graph_s* g);
 int64_t component_tuples_impl(bfs_graph_s* g);
+// validate.cu
+void validate_impl(bfs_graph_s* g, int64_t root, const int32_t* parent, const int32_t* depth, int64_t fails[5]);
 void sample_roots_impl(bfs_graph_s* g, uint32_t scale, uint64_t seed, int64_t count, int64_t* roots, int64_t* found);
 // host-side Philox (product's own; used for root candidates)
 void philox4x32_10_host(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -96,3 +96,18 @@ def test_hot_kernel_resource_budget(so):
         assert stack <= 16, (reg, stack)         # no real spilling
     for reg, stack in td_multi:                  # p ranks: the remote-claim path adds a small spill
         assert 48 < reg <= 64 and stack <= 64, (reg, stack)
+
+
+def test_output_buffer_checks():
+    """bfs_run's binding rejects buffers the C call would overrun or misread."""
+    import numpy as np
+    import torch
+    import paper_1503_04359_b200 as pkg
+    ok = torch.empty(10, dtype=torch.int32)
+    pkg._check_output(ok, 10, "x")
+    pkg._check_output(np.empty(12, np.int32), 10, "x")
+    pkg._check_output(None, 10, "x")
+    for bad in (torch.empty(10, dtype=torch.int64), torch.empty(9, dtype=torch.int32),
+                torch.empty(20, dtype=torch.int32)[::2], np.empty(10, np.int64), np.empty(5, np.int32), [0] * 10):
+        with pytest.raises(ValueError):
+            pkg._check_output(bad, 10, "x")

@@ -23,19 +23,20 @@ def _run(args, timeout):
 
 @pytest.mark.timeout(600)
 def test_reference_arm_line():
-    d = _run(["--impl", "reference", "--steps", "1", "--warmup", "0"], 560)
+    d = _run(["--impl", "reference", "--steps", "2", "--warmup", "0", "--cpu-scale", "16"], 560)
     assert BASE_KEYS <= set(d) and d["impl"] == "reference"
     assert d["value"] > 0 and d["unit"] == "GTEPS" and d["higher_is_better"] is True
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] == d["value"]
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+    assert d["config"]["sample_scale"] == 16 and d["cpu_baseline"]["cores"] >= 1
 
 
 @pytest.mark.gpu
 @pytest.mark.timeout(900)
 def test_our_arm_line_k16():
-    d = _run(["--config", "k16", "--steps", "1", "--warmup", "3"], 850)
+    d = _run(["--config", "k16", "--steps", "1", "--warmup", "0"], 850)
     assert BASE_KEYS <= set(d) and "impl" not in d
-    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 3
+    assert d["value"] > 0 and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 0
     assert d["config"]["workload"].startswith("Graph500 Kronecker scale 16")
     rl = d["roofline"]
     assert rl["bound"] == "hbm" and rl["peak"] > 0 and abs(rl["frac"] - rl["achieved"] / rl["peak"]) < 1e-3
@@ -43,3 +44,5 @@ def test_our_arm_line_k16():
     assert d["e2e"]["value"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert "sm_mhz" in d["clocks"]
+    v = d["validation"]
+    assert v["searches"] == 64 and v["failed_searches"] == 0 and v["rules"] == {}

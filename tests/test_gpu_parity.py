@@ -393,3 +393,54 @@ def test_claim_only_topdown_steps(loop, monkeypatch):
         _check_outputs(g, ref, int(r), dict(loop=loop, mode=1))
         _check_outputs(g, ref, int(r), dict(loop=loop, mode=0, alpha=30, beta=1000))
     g.close()
+
+
+def test_persistent_grid_not_coresident_falls_back(monkeypatch):
+    """The persistent search is a cooperative launch (its grid barrier needs every CTA
+    resident).  A grid that cannot be co-resident must fail the launch, and the search
+    must then run as the loop graph with identical results -- never hang."""
+    uv, ref = oracle.kron_graph(12, 16, 4)
+    g = pkg.Graph.kronecker(12, 16, 4)
+    roots = [int(r) for r in g.sample_roots(12, 4, 3)]
+    monkeypatch.setenv("BFS_PERSIST_GRID", str(1 << 20))
+    for r in roots:
+        _check_run(g, ref, r, dict(mode=0, loop="persistent"), uv)
+    monkeypatch.delenv("BFS_PERSIST_GRID")
+    for r in roots:
+        _check_run(g, ref, r, dict(mode=0, loop="persistent"), uv)
+    g.close()
+
+
+@pytest.mark.parametrize("reindex,rows", [(False, 1), (True, 1), (False, 2), (False, 0)])
+def test_device_validator_matches_oracle_validator(reindex, rows):
+    """bfs_validate (the bench's self-check) flags exactly the rules the oracle's CSR
+    validator flags: on the GPU's own outputs (none) and on corrupted copies."""
+    rng = np.random.default_rng(5 + rows)
+    uv, _ = oracle.kron_graph(12, 16, 6)
+    ref = oracle.build_csr(1 << 12, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    g = pkg.Graph.kronecker(12, 16, 6, opts=pkg.default_opts(reindex_by_degree=reindex, sort_rows=rows))
+    for r in g.sample_roots(12, 6, 4):
+        r = int(r)
+        parent, depth = g.run(r)
+        assert pkg.bfs_validate(g.h, r, parent, depth) == {}
+        d0, p0 = depth.cpu().numpy(), parent.cpu().numpy()
+        for kind in range(6):
+            d, p = d0.copy(), p0.copy()
+            v = int(rng.choice(np.flatnonzero(d0 > 1)))
+            if kind == 0:
+                p[v] = r                          # V2 + V3
+            elif kind == 1:
+                d[v], p[v] = -1, -1               # V4 (S:370)
+            elif kind == 2:
+                p[r] = v                          # V1
+            elif kind == 3:
+                d[v] += 1                         # V3 / V4
+            elif kind == 4:
+                p[v] = -1                         # V5
+            else:
+                d[v] = 0                          # V1 + V3 + V4
+            want = {k for k in oracle.validate(ref, r, d, p) if k != "V6_exact_depth"}
+            got = set(pkg.bfs_validate(g.h, r, torch.from_numpy(p).cuda(), torch.from_numpy(d).cuda()))
+            assert got == want, (kind, got, want)
+            assert set(pkg.bfs_validate(g.h, r, p, d)) == want          # host buffers
+    g.close()
