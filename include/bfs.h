@@ -174,6 +174,13 @@ bfs_status bfs_graph_info(bfs_graph_t g, int64_t* n, int64_t* arcs, int64_t* loc
  * owned range.  Lets measurements charge bitmap bytes per launch exactly. */
 bfs_status bfs_graph_active(bfs_graph_t g, int64_t* n_active);
 
+/* Tiled top-down index (degree-reindexed graphs on one GPU):
+ * *heavy_rows = rows [0, heavy_rows) whose frontier arcs a tile-mode top-down step
+ * expands per label tile in shared memory, *tiles = number of label tiles (0: no
+ * index, every top-down step uses the edge-balanced expansion), *build_ms = device
+ * time of the index build (included in bfs_graph_build_ms).  Any pointer may be NULL. */
+bfs_status bfs_graph_tiles(bfs_graph_t g, int64_t* heavy_rows, int64_t* tiles, double* build_ms);
+
 /* Construction time of the last bfs_graph_create on this handle (device ms). */
 bfs_status bfs_graph_build_ms(bfs_graph_t g, double* ms);
 

@@ -33,7 +33,7 @@ EXPORTS = ("bfs_graph_create", "bfs_graph_create_kronecker", "bfs_graph_create_e
            "bfs_comm_unique_id", "bfs_comm_create", "bfs_comm_create_local", "bfs_comm_destroy", "bfs_last_error",
            "bfs_kronecker_edges", "bfs_graph_export_csr", "bfs_graph_export_labels", "bfs_sample_roots",
            "bfs_set_allocator", "bfs_abi_version", "bfs_partition_range", "bfs_graph_export_row", "bfs_component_tuples",
-           "bfs_validate", "bfs_graph_active")
+           "bfs_validate", "bfs_graph_active", "bfs_graph_tiles")
 
 
 class BfsError(RuntimeError):
@@ -115,6 +115,7 @@ def lib() -> ctypes.CDLL:
             "bfs_component_tuples": [P, P],
             "bfs_validate": [P, i64, P, P, P],
             "bfs_graph_active": [P, P],
+            "bfs_graph_tiles": [P, P, P, P],
         }
         for name, args in sig.items():
             f = getattr(L, name)
@@ -195,6 +196,13 @@ def bfs_graph_active(h) -> int:
     x = ctypes.c_int64()
     _check(lib().bfs_graph_active(h, ctypes.byref(x)))
     return x.value
+
+
+def bfs_graph_tiles(h) -> dict:
+    """Tiled top-down index: heavy rows, label tiles (0 = none), index build ms."""
+    hr, t, ms = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_double()
+    _check(lib().bfs_graph_tiles(h, ctypes.byref(hr), ctypes.byref(t), ctypes.byref(ms)))
+    return {"heavy_rows": hr.value, "tiles": t.value, "build_ms": ms.value}
 
 
 def bfs_graph_build_ms(h) -> float:

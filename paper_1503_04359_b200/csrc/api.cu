@@ -187,6 +187,7 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
     BFS_CUDA(cudaEventCreate(&e1));
     BFS_CUDA(cudaEventRecord(e0, g->stream));
     build_graph(g, &d);
+    bfs_build_tiles(g);   // tiled top-down index (eligible graphs only)
     if (comm && comm->nranks > 1) {
         // global arc count for the switch rule (m_u)
         DevBuf<int64_t> a;
@@ -278,6 +279,15 @@ bfs_status bfs_graph_active(bfs_graph_t g, int64_t* n_active) {
     if (!g || !n_active) fail(BFS_ERR_INVALID_ARG, "NULL argument");
     const bool active = g->reindexed && !(g->comm && g->comm->nranks > 1) && g->nparts == 1;
     *n_active = active ? g->n_active : g->nl();
+    API_END
+}
+
+bfs_status bfs_graph_tiles(bfs_graph_t g, int64_t* heavy_rows, int64_t* tiles, double* build_ms) {
+    API_BEGIN
+    if (!g) fail(BFS_ERR_INVALID_ARG, "graph is NULL");
+    if (heavy_rows) *heavy_rows = g->tile_T ? g->tile_nh : 0;
+    if (tiles) *tiles = g->tile_T;
+    if (build_ms) *build_ms = g->tile_build_ms;
     API_END
 }
 

@@ -39,6 +39,7 @@ namespace bfsb {
 namespace {
 
 #include "bfs_common.cuh"
+#include "td_tile.cuh"
 #include "bfs_steps.cuh"
 #include "bfs_loop.cuh"
 
@@ -89,7 +90,155 @@ int td_resident_grid() {
 
 bool multi(const bfs_graph_s* g) { return g->comm && g->comm->nranks > 1; }
 
+// tiled top-down (td_tile.cuh) knobs; the BFS_TILE* variables are for tuning and tests
+static int64_t env_i64(const char* name, int64_t dflt) {
+    const char* e = getenv(name);
+    return e && *e ? atoll(e) : dflt;
+}
+// top-down steps with at least this many arcs run tiled when the graph has a tile index
+static int64_t tile_min_setting() { return env_i64("BFS_TILE_MIN", (int64_t)1 << 24); }
+
+TileLog tile_log(const bfs_graph_s* g) {
+    return TileLog{g->tile_pool.p, g->tile_ubase.p, g->tile_ucnt.p, g->tile_lpool.p, g->tile_lcnt.p,
+                   g->tile_start.p, g->tile_wf.p, g->tile_T};
+}
+
 }  // namespace
+
+// The tile index of td_tile.cuh for a degree-reindexed graph on one GPU: heavy rows
+// [0, nh) are those of degree >= H (the reindex orders labels by decreasing degree, so
+// they form a prefix); tiles of about equal arc mass, each at most `maxw` visited
+// words; per heavy row and tile the first arc into the tile (k_tile_bnd).
+void bfs_build_tiles(bfs_graph_s* g) {
+    g->tile_T = 0;
+    g->tile_nh = 0;
+    if (!active_range(g) || env_i64("BFS_TILE", 1) == 0) return;
+    cudaStream_t s = g->stream;
+    const int64_t na = g->n_active;
+    if (na < 64) return;
+    auto degree = [&](int64_t v) {
+        int64_t b[2];
+        BFS_CUDA(cudaMemcpy(b, g->off.p + v, 2 * sizeof(int64_t), cudaMemcpyDeviceToHost));
+        return b[1] - b[0];
+    };
+    // offsets sampled at every word boundary (32 labels), plus the end
+    const int64_t step = 32;
+    const int64_t K = (na + step - 1) / step;
+    std::vector<int64_t> so((size_t)K + 1);
+    {
+        DevBuf<int64_t> d;
+        d.alloc((size_t)K, s);
+        k_gather_stride<<<grid_for(K, 256), 256, 0, s>>>(g->off.p, step, K, d.p);
+        BFS_CHECK_LAUNCH();
+        BFS_CUDA(cudaMemcpyAsync(so.data(), d.p, (size_t)K * 8, cudaMemcpyDeviceToHost, s));
+        BFS_CUDA(cudaMemcpyAsync(&so[K], g->off.p + na, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        BFS_CUDA(cudaStreamSynchronize(s));
+    }
+    const int64_t maxw = std::max<int64_t>(1, std::min<int64_t>(env_i64("BFS_TILE_WORDS", kTileMaxWordsDefault),
+                                                                std::min(48 * 1024, kMaxWin * kWin / 32)));
+    const int64_t vmax = maxw * 32;
+    const int64_t target = std::max<int64_t>(1, env_i64("BFS_TILE_COUNT", 4 * (int64_t)num_sms()));
+    const int64_t mass = std::max<int64_t>(1, (so[K] - so[0]) / target);
+    std::vector<int32_t> ts{0};
+    int64_t cur = 0;
+    for (int64_t k = 1; k < K; ++k)
+        if (so[k] - so[cur] >= mass || (k + 1 - cur) * step > vmax) {
+            ts.push_back((int32_t)(k * step));
+            cur = k;
+        }
+    ts.push_back((int32_t)(words_of(na) * 32));
+    const int T = (int)ts.size() - 1;
+    if (T > 16384) return;   // k_tile_bnd keeps the starts in shared memory
+    // work units: a tile heavier than the mass target is split over up to 64 CTAs
+    // (only tiles of at most maxw/2 words: a split part keeps a second copy of its words)
+    std::vector<int2> units;
+    int64_t wmax = 0;
+    for (int t = 0; t < T; ++t) {
+        const int64_t w = (ts[t + 1] - ts[t]) / 32;
+        const int64_t m = so[std::min<int64_t>(K, ts[t + 1] / step)] - so[ts[t] / step];
+        int parts = (int)std::min<int64_t>(64, std::max<int64_t>(1, (m + mass - 1) / mass));
+        if (2 * w > maxw) parts = 1;
+        for (int q = 0; q < parts; ++q) units.push_back(make_int2(t, q | (parts << 16)));
+        wmax = std::max<int64_t>(wmax, parts > 1 ? 2 * w : w);
+    }
+    // heavy rows: degree >= H (binary search on the non-increasing degrees); H doubles
+    // until the table fits the budget
+    const int64_t budget = env_i64("BFS_TILE_BUDGET", (int64_t)8 << 30);
+    int64_t H = std::max<int64_t>(1, env_i64("BFS_TILE_H", 4096)), nh = 0;
+    for (;;) {
+        int64_t lo = 0, hi = na;   // first label with degree < H
+        while (lo < hi) {
+            const int64_t m = (lo + hi) / 2;
+            if (degree(m) >= H) lo = m + 1;
+            else hi = m;
+        }
+        nh = lo;
+        if (nh * (int64_t)(T + 1) * 4 <= budget) break;
+        H *= 2;
+    }
+    if (nh == 0) return;
+    cudaEvent_t e0, e1;
+    BFS_CUDA(cudaEventCreate(&e0));
+    BFS_CUDA(cudaEventCreate(&e1));
+    BFS_CUDA(cudaEventRecord(e0, s));
+    g->tile_start.alloc((size_t)T + 1, s);
+    BFS_CUDA(cudaMemcpyAsync(g->tile_start.p, ts.data(), (size_t)(T + 1) * 4, cudaMemcpyHostToDevice, s));
+    g->tile_unit.alloc(units.size(), s);
+    BFS_CUDA(cudaMemcpyAsync(g->tile_unit.p, units.data(), units.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+    g->tile_bnd.alloc((size_t)nh * (T + 1), s);
+    g->tile_hlist.alloc((size_t)nh, s);
+    g->tile_hcnt.alloc(1, s);
+    // record log: unit u owns one kWin-entry bucket per window of its tile
+    {
+        std::vector<int64_t> ub(units.size());
+        std::vector<int32_t> fu((size_t)T, -1), wf((size_t)T, 0);
+        std::vector<int2> wl;
+        int64_t tot = 0;
+        for (size_t u = 0; u < units.size(); ++u) {
+            const int t = units[u].x;
+            const int64_t nwin = ((int64_t)ts[t + 1] - ts[t] + kWin - 1) / kWin;
+            ub[u] = tot;
+            tot += nwin * kWin;
+            if (fu[t] < 0) {
+                fu[t] = (int32_t)u;
+                wf[t] = (int32_t)wl.size();
+                for (int k = 0; k < nwin; ++k) wl.push_back(make_int2(t, k));
+            }
+        }
+        g->tile_pool.alloc((size_t)tot, s);
+        g->tile_ubase.alloc(ub.size(), s);
+        g->tile_ucnt.alloc(units.size() * kMaxWin, s);
+        g->tile_wl.alloc(wl.size(), s);
+        g->tile_fu.alloc((size_t)T, s);
+        g->tile_wf.alloc((size_t)T, s);
+        g->tile_lpool.alloc(wl.size() * kWin, s);
+        g->tile_lcnt.alloc(wl.size(), s);
+        BFS_CUDA(cudaMemcpyAsync(g->tile_wf.p, wf.data(), wf.size() * 4, cudaMemcpyHostToDevice, s));
+        BFS_CUDA(cudaMemcpyAsync(g->tile_ubase.p, ub.data(), ub.size() * 8, cudaMemcpyHostToDevice, s));
+        BFS_CUDA(cudaMemcpyAsync(g->tile_wl.p, wl.data(), wl.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        BFS_CUDA(cudaMemcpyAsync(g->tile_fu.p, fu.data(), fu.size() * 4, cudaMemcpyHostToDevice, s));
+        BFS_CUDA(cudaStreamSynchronize(s));   // the host vectors go out of scope
+        g->tile_nwl = (int)wl.size();
+    }
+    BFS_CUDA(cudaFuncSetAttribute(k_tile_rec, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kWin * 4)));
+    const size_t smem_bnd = (size_t)(T + 1) * 4;
+    if (smem_bnd > 48 * 1024)
+        BFS_CUDA(cudaFuncSetAttribute(k_tile_bnd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bnd));
+    k_tile_bnd<<<grid_for(nh * 32, 256), 256, smem_bnd, s>>>(g->off.p, g->adj.p, g->tile_start.p, T, nh, g->tile_bnd.p);
+    BFS_CHECK_LAUNCH();
+    BFS_CUDA(cudaFuncSetAttribute(k_td_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(wmax * 4)));
+    BFS_CUDA(cudaEventRecord(e1, s));
+    BFS_CUDA(cudaEventSynchronize(e1));
+    float ms = 0;
+    BFS_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    g->tile_build_ms = ms;
+    g->tile_T = T;
+    g->tile_units = (int)units.size();
+    g->tile_nh = nh;
+    g->tile_maxw = (int)wmax;
+}
 
 void bfs_alloc_state(bfs_graph_s* g) {
     cudaStream_t s = g->stream;
@@ -255,24 +404,37 @@ static void build_loop_graph(bfs_graph_s* g) {
     cudaGraph_t U = add_cond(B, {n_begin}, h_bu, cudaGraphCondTypeIf, &n_bu);
     add_kernel(B, {n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
     // top-down body
+    unsigned* hcnt = g->tile_T ? g->tile_hcnt.p : nullptr;
+    const TileLog lg = tile_log(g);
     cudaGraphNode_t t1 = add_kernel(T, {}, k_td_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words, g->head.p, qa, qb,
-                                    cnt, tstate, g->tctr.p, (const uint32_t*)g->visited.p);
+                                    cnt, tstate, g->tctr.p, (const uint32_t*)g->visited.p, hcnt, g->tile_lcnt.p,
+                                    (int64_t)g->tile_nwl);
     cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, (int64_t)0, g->prefix.p,
-                                    tstate, g->tctr.p);
+                                    tstate, g->tctr.p, g->tile_nh, g->tile_hlist.p, hcnt, 0);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
                                     g->scratch64.p, ctl);
     cudaGraphNode_t t4 = add_kernel(T, {t3}, k_td_expand<false>, dim3(td_resident_grid<false>()), dim3(kTdThreads), 0,
                                     qa, g->prefix.p, g->scratch64.p, (int64_t)0, (int64_t)0, g->off.p, g->adj.p,
                                     g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo, g->hi, Remote{},
-                                    ctl, lrec, -1);
+                                    ctl, lrec, -1, lg);
+    if (g->tile_T) {   // heavy frontier rows and the records of a tile-mode step (return at once otherwise)
+        t4 = add_kernel(T, {t4}, k_td_tile, dim3(g->tile_units), dim3(kTileThreads), (size_t)g->tile_maxw * 4,
+                        (const Ctl*)ctl, (const int32_t*)g->tile_start.p, g->tile_T, (const int2*)g->tile_unit.p,
+                        (const int32_t*)g->tile_bnd.p, (const int32_t*)g->tile_hlist.p, (const unsigned*)hcnt,
+                        (const int64_t*)g->off.p, (const int32_t*)g->adj.p, g->visited.p, pmap, lg, lrec);
+        t4 = add_kernel(T, {t4}, k_tile_rec, dim3(g->tile_nwl), dim3(kWinThreads), (size_t)kWin * 4, (const Ctl*)ctl,
+                        (int32_t)0, (const int2*)g->tile_wl.p, (const int32_t*)g->tile_fu.p,
+                        (const int2*)g->tile_unit.p, lg, (const uint32_t*)g->visited.p, (const uint32_t*)g->front.p,
+                        (const uint32_t*)g->next.p, g->rec.p, lrec);
+    }
+    const int64_t nbatches = (words + 31) / 32;
+    const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
+    const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
     add_kernel(T, {t4}, k_td_finish_dev, g8, t256, 0, ctl, (const uint32_t*)g->visited.p, g->front.p, g->next.p, words,
                g->head.p, qa, qb, cnt);
     // bottom-up body
     cudaGraphNode_t u1 = add_kernel(U, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
     cudaGraphNode_t u2 = add_kernel(U, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
-    const int64_t nbatches = (words + 31) / 32;
-    const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
-    const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
     add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
                g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
                cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
@@ -354,7 +516,8 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
     k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
                                                  g->rec.p, qa, g->head.p, (unsigned long long*)g->cnt.p, ctl, g->policy,
-                                                 g->n, g->arcs_global, kGraphMaxLevels, td_claim_min());
+                                                 g->n, g->arcs_global, kGraphMaxLevels, td_claim_min(),
+                                                 (persistent || !g->tile_T) ? (int64_t)-1 : tile_min_setting());
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
     if (persistent) {
@@ -449,7 +612,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             comp += L.kernel_ms;
         }
         g->levels.push_back(L);
-        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 5 : 3);
+        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 5 + (g->tile_T ? 2 : 0) : 3);
     }
     float ms = 0, ms_init = 0, ms_loop = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
@@ -612,17 +775,29 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 BFS_CUDA(cudaMemsetAsync(g->out_cnt.p, 0, (size_t)p * sizeof(int64_t), s));
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
+            // tile mode (td_tile.cuh): heavy frontier rows expanded per tile, the rest below
+            const bool tile_mode = !mg && g->tile_T > 0 && E >= tile_min_setting();
             if (E > 0) {
                 l2_window(g, g->visited.p, g->visited.bytes());
                 // single-pass scan of the queue degrees (the loop graph's kernel, host-sized)
                 BFS_CUDA(cudaMemsetAsync(g->tstate.p, 0, (size_t)((nf_loc + kScanTile - 1) / kScanTile) * 8, s));
                 BFS_CUDA(cudaMemsetAsync(g->tctr.p, 0, sizeof(uint32_t), s));
+                if (tile_mode) {
+                    BFS_CUDA(cudaMemsetAsync(g->tile_hcnt.p, 0, sizeof(uint32_t), s));
+                    BFS_CUDA(cudaMemsetAsync(g->tile_lcnt.p, 0, (size_t)g->tile_nwl * 4, s));
+                }
+                const TileLog lg = tile_mode ? tile_log(g) : TileLog{};
                 k_scan_dev<<<grid_for((nf_loc + kScanTile - 1) / kScanTile * kScanThreads, kScanThreads), kScanThreads, 0,
                              s>>>(nullptr, qcur, qcur, nf_loc, g->prefix.p, (unsigned long long*)g->tstate.p,
-                                  g->tctr.p);
+                                  g->tctr.p, g->tile_nh, g->tile_hlist.p, g->tile_hcnt.p, tile_mode ? 1 : 0);
                 BFS_CHECK_LAUNCH();
                 ++launches;
-                const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
+                int64_t El = E;   // arcs of the edge-balanced expansion (tile mode: light rows)
+                if (tile_mode) {
+                    BFS_CUDA(cudaMemcpyAsync(&El, g->prefix.p + nf_loc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                    BFS_CUDA(cudaStreamSynchronize(s));
+                }
+                const int64_t nchunks = (El + kTdChunk - 1) / kTdChunk;
                 k_td_chunk_starts<<<grid_for(nchunks, 256), 256, 0, s>>>(g->prefix.p, nf_loc, nchunks, g->scratch64.p,
                                                                           nullptr);
                 BFS_CHECK_LAUNCH();
@@ -630,13 +805,26 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 // large single-partition steps: claims + records only, the winners' degrees
                 // and the next queue from k_td_finish in vertex order (visited snapshot in
                 // `next`, which becomes the next frontier bitmap)
-                claim_mode = !mg && E >= td_claim_min();
+                claim_mode = !mg && (E >= td_claim_min() || tile_mode);
                 if (claim_mode) {
                     BFS_CUDA(cudaMemcpyAsync(next, g->visited.p, (size_t)words * 4, cudaMemcpyDeviceToDevice, s));
-                    k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
-                                                                   g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
-                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr, 1);
-                    BFS_CHECK_LAUNCH();
+                    if (El > 0) {
+                        k_td_expand<false><<<std::max(1, grid), kTdThreads, 0, s>>>(
+                            qcur, g->prefix.p, g->scratch64.p, nf_loc, El, g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt,
+                            g->head.p, cnt, d + 1, g->lo, g->hi, rm, nullptr, nullptr, tile_mode ? 2 : 1, lg);
+                        BFS_CHECK_LAUNCH();
+                    }
+                    if (tile_mode) {
+                        k_td_tile<<<g->tile_units, kTileThreads, (size_t)g->tile_maxw * 4, s>>>(
+                            nullptr, g->tile_start.p, g->tile_T, g->tile_unit.p, g->tile_bnd.p, g->tile_hlist.p,
+                            g->tile_hcnt.p, g->off.p, g->adj.p, g->visited.p, pmap, lg, nullptr);
+                        BFS_CHECK_LAUNCH();
+                        k_tile_rec<<<g->tile_nwl, kWinThreads, (size_t)kWin * 4, s>>>(
+                            nullptr, (int32_t)(d + 1), g->tile_wl.p, g->tile_fu.p, g->tile_unit.p, lg, g->visited.p,
+                            next, nullptr, rec, nullptr);
+                        BFS_CHECK_LAUNCH();
+                        launches += 2;
+                    }
                     k_td_finish<<<grid_for(words * 32, 256), 256, 0, s>>>(g->visited.p, next, words, g->head.p, qnxt,
                                                                          cnt);
                     BFS_CHECK_LAUNCH();
@@ -644,11 +832,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 } else if (mg)
                     k_td_expand<true><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E, g->off.p,
                                                                   g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt, d + 1,
-                                                                  g->lo, g->hi, rm, nullptr, nullptr, 0);
+                                                                  g->lo, g->hi, rm, nullptr, nullptr, 0, TileLog{});
                 else
                     k_td_expand<false><<<grid, kTdThreads, 0, s>>>(qcur, g->prefix.p, g->scratch64.p, nf_loc, E,
                                                                    g->off.p, g->adj.p, g->visited.p, rec, pmap, qnxt, g->head.p, cnt,
-                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr, 0);
+                                                                   d + 1, g->lo, g->hi, rm, nullptr, nullptr, 0, TileLog{});
                 BFS_CHECK_LAUNCH();
                 launches += 2;
             }

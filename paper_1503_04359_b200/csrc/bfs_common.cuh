@@ -58,6 +58,8 @@ struct Ctl {
     int mode, bu_from, max_levels, done;   // done: the persistent kernel's stop flag
     long long claim_min;      // top-down steps with at least this many arcs run claim-only
     int claim, front_ok;      // this step is claim-only; the front bitmap holds the frontier
+    long long tile_min;       // top-down steps with at least this many arcs run tiled (< 0: no tile index)
+    int tile, tile_pad;       // this step runs tiled (td_tile.cuh; implies claim)
 };
 // one record per step, filled by the step kernels (times: %globaltimer ns)
 struct LevelRec {

@@ -17,7 +17,8 @@
 __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip, int64_t pw,
                            int64_t root, const int32_t* __restrict__ label, int2* __restrict__ out, Queue q,
                            const int2* __restrict__ head, unsigned long long* __restrict__ cnt, Ctl* ctl,
-                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels, int64_t claim_min) {
+                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels, int64_t claim_min,
+                           int64_t tile_min) {
     const int64_t ri = label ? (int64_t)__ldg(label + root) : root;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
@@ -42,6 +43,7 @@ __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __res
         c.bu_from = pol.bu_from_level;
         c.max_levels = max_levels;
         c.claim_min = claim_min;
+        c.tile_min = tile_min;
         *ctl = c;
     }
 }
@@ -95,6 +97,7 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
         c.front_ok = 0;
     }
     c.claim = 0;
+    c.tile = 0;
     c.prev_nf = c.n_f;
     c.n_f = next;
     c.m_f = c.m_fc = mf;
@@ -114,7 +117,8 @@ __global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, 
     const long long m_u = step_decide(c);
     c.E = c.m_f;
     c.nchunks = (c.E + kTdChunk - 1) / kTdChunk;
-    c.claim = c.dir == 0 && c.E >= c.claim_min;
+    c.tile = c.dir == 0 && c.tile_min >= 0 && c.E >= c.tile_min;
+    c.claim = c.dir == 0 && (c.E >= c.claim_min || c.tile);
     LevelRec r{};
     r.n_f = c.n_f;
     r.m_f = c.m_f;
@@ -141,11 +145,19 @@ __global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* c
 __global__ void k_td_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* __restrict__ f1,
                           int64_t words, const int2* __restrict__ head, Queue qa, Queue qb,
                           unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ tstate,
-                          unsigned int* __restrict__ tctr, const uint32_t* __restrict__ visited) {
+                          unsigned int* __restrict__ tctr, const uint32_t* __restrict__ visited,
+                          unsigned* __restrict__ hcount, unsigned* __restrict__ lcnt, int64_t nwl) {
     const int64_t tiles = (ctl->n_f + 2047) / 2048;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tiles; i += (int64_t)gridDim.x * blockDim.x)
         tstate[i] = 0ull;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *tctr = 0u;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        *tctr = 0u;
+        if (hcount) *hcount = 0u;   // heavy list (tile mode)
+    }
+    if (ctl->tile && lcnt)   // light-row record buckets (tile mode)
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwl; i += (int64_t)gridDim.x * blockDim.x)
+            lcnt[i] = 0u;
+
     if (ctl->claim) {   // claim-only step: snapshot visited into the spare bitmap (k_td_finish)
         uint32_t* snap = ctl->fsel ? f0 : f1;
         for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x)
@@ -167,14 +179,19 @@ __global__ void k_td_finish_dev(const Ctl* ctl, const uint32_t* __restrict__ vis
 constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kScanItems;
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
+// Tile mode (td_tile.cuh): queue entries with label < nh (heavy rows) count 0 arcs
+// here -- the tiled kernel expands them -- and are listed in hlist (count *hcount).
 __global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue qa, Queue qb, int64_t n_host,
                                                            int64_t* __restrict__ out, unsigned long long* tstate,
-                                                           unsigned int* tctr) {
+                                                           unsigned int* tctr, int64_t nh, int32_t* __restrict__ hlist,
+                                                           unsigned* __restrict__ hcount, int tile_host) {
     __shared__ long long s_tile, s_excl;
     __shared__ long long s_warp[kScanThreads / 32];
     // loop graph: size and queue from the loop state; host loop: qa holds the queue
     const long long n = ctl ? ctl->n_f : n_host;
     const int32_t* __restrict__ deg = (ctl && ctl->qsel) ? qb.deg : qa.deg;
+    const int32_t* __restrict__ qv = (ctl && ctl->qsel) ? qb.v : qa.v;
+    const bool tile = ctl ? ctl->tile != 0 : tile_host != 0;
     const long long tiles = (n + kScanTile - 1) / kScanTile;
     if (n == 0) {
         if (blockIdx.x == 0 && threadIdx.x == 0) out[0] = 0;
@@ -191,6 +208,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
             v[k] = base + k < n ? (long long)deg[base + k] : 0;
+            if (tile) {
+                const int32_t u = base + k < n ? qv[base + k] : INT32_MAX;
+                const bool heavy = u < nh;
+                const unsigned m = __ballot_sync(kFull, heavy);
+                if (m) {
+                    unsigned pos = 0;
+                    if (lane == __ffs(m) - 1) pos = atomicAdd(hcount, (unsigned)__popc(m));
+                    pos = __shfl_sync(kFull, pos, __ffs(m) - 1);
+                    if (heavy) hlist[pos + __popc(m & lanemask_lt())] = u;
+                }
+                if (heavy) v[k] = 0;
+            }
             sum += v[k];
         }
         long long inc = sum;

@@ -28,9 +28,9 @@ __global__ void k_init(uint32_t* visited, const uint32_t* skip, int64_t pw, int6
 // chunk c of the top-down arc range starts inside frontier entry starts[c]
 __global__ void k_td_chunk_starts(const int64_t* prefix, int64_t F, int64_t nchunks, int64_t* starts,
                                   const Ctl* ctl) {
-    if (ctl) {
+    if (ctl) {   // E = prefix[F]: the arcs this expansion covers (tile mode: light rows only)
         F = ctl->n_f;
-        nchunks = ctl->nchunks;
+        nchunks = (prefix[F] + kTdChunk - 1) / kTdChunk;
     }
     for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nchunks; c += (int64_t)gridDim.x * blockDim.x) {
         const int64_t e = c * kTdChunk;
@@ -66,7 +66,8 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
             int64_t F, int64_t E, const int64_t* __restrict__ off, const int32_t* __restrict__ adj,
             uint32_t* __restrict__ visited, int2* __restrict__ out, const int32_t* __restrict__ pmap,
             const Queue qnext_in, const int2* __restrict__ head, unsigned long long* __restrict__ cnt,
-            int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec, int claim_only_in) {
+            int32_t next_level, int64_t lo, int64_t hi, Remote rm, const Ctl* ctl, LevelRec* lrec, int claim_only_in,
+            TileLog lg) {
     __shared__ int64_t s_pre[kTdStage + 2];
     __shared__ int64_t s_beg[kTdStage + 1];
     __shared__ int32_t s_u[kTdStage + 1];
@@ -79,13 +80,15 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
     Queue qc = q_in, qnext = qnext_in;
     if (ctl) {   // device-driven loop: sizes and queue selector from the loop state
         F = ctl->n_f;
-        E = ctl->E;
+        E = prefix[F];   // = m_f, or the light rows' arcs in tile mode
         next_level = ctl->d + 1;
         if (ctl->qsel) { qc = qnext_in; qnext = q_in; }
         stamp_begin(lrec, ctl);
     }
     const Queue q = qc;
     const bool claim_only = claim_only_in > 0 || (claim_only_in < 0 && ctl && ctl->claim);   // < 0: the loop state decides
+    // tile mode: the winners' records go to the (tile, window) buckets (k_tile_rec stores them)
+    const bool use_log = lg.lpool && (claim_only_in == 2 || (claim_only_in < 0 && ctl && ctl->tile));
     const int64_t nchunks = (E + kTdChunk - 1) / kTdChunk;
     if (threadIdx.x == 0) s_qn = 0;
     for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -184,9 +187,15 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         // -- only the claiming thread knows the parent -- but their degrees and the next
         // queue are produced in vertex order by k_td_finish
         if (claim_only) {
+            if (use_log) {
 #pragma unroll
-            for (int j = 0; j < kTdItems; ++j)
-                if (win[j]) __stcs(out + (v[j] - lo), make_int2(next_level, pmap ? __ldg(pmap + u[j]) : u[j]));
+                for (int j = 0; j < kTdItems; ++j)
+                    light_log(lg, win[j], v[j], win[j] ? (pmap ? __ldg(pmap + u[j]) : u[j]) : 0);
+            } else {
+#pragma unroll
+                for (int j = 0; j < kTdItems; ++j)
+                    if (win[j]) __stcs(out + (v[j] - lo), make_int2(next_level, pmap ? __ldg(pmap + u[j]) : u[j]));
+            }
             __syncthreads();
             continue;
         }

@@ -173,6 +173,29 @@ struct bfs_graph_s {
     int64_t* h_ctl = nullptr;
     int64_t* h_lrec = nullptr;
 
+    // tiled top-down (td_tile.cuh; degree-reindexed graphs on one GPU): heavy rows
+    // [0, tile_nh), tile_T tiles of internal labels, per heavy row the first arc of
+    // each tile; tile_T == 0: no index (tile mode off)
+    int64_t tile_nh = 0;
+    int tile_T = 0, tile_maxw = 0;
+    int tile_units = 0;
+    bfsb::DevBuf<int32_t> tile_start;  // [T + 1] first label of each tile (multiples of 32), then the end
+    bfsb::DevBuf<int2> tile_unit;      // [units] (tile, part | parts << 16): hub tiles split over several CTAs
+    bfsb::DevBuf<int32_t> tile_bnd;    // [nh * (T + 1)]
+    bfsb::DevBuf<int32_t> tile_hlist;  // [nh] heavy frontier vertices of the current step
+    bfsb::DevBuf<uint32_t> tile_hcnt;  // [1] heavy-list length
+    // tile-mode record log (td_tile.cuh): per unit one bucket per 2^kWinShift-label window
+    int tile_nwl = 0;                  // (tile, window) pairs
+    bfsb::DevBuf<int2> tile_pool;      // (vertex, parent) entries
+    bfsb::DevBuf<int64_t> tile_ubase;  // [units] first entry of each unit's buckets
+    bfsb::DevBuf<uint32_t> tile_ucnt;  // [units * kMaxWin] entries per bucket
+    bfsb::DevBuf<int2> tile_wl;        // [nwl] (tile, window)
+    bfsb::DevBuf<int32_t> tile_fu;     // [T] first unit of each tile
+    bfsb::DevBuf<int32_t> tile_wf;     // [T] first (tile, window) index of each tile
+    bfsb::DevBuf<int2> tile_lpool;     // [nwl * kWin] light-row winners per (tile, window)
+    bfsb::DevBuf<uint32_t> tile_lcnt;  // [nwl]
+    double tile_build_ms = 0;
+
     bfs_policy policy{0, 15, 18, 0, 0, 0};
     bfsb::DevBuf<int32_t> big;       // persistent kernel: big frontier rows of a top-down step
     bfsb::DevBuf<int64_t> pcnt;      // persistent kernel: three counter sets
@@ -196,6 +219,7 @@ void kron_edges_device(const bfs_kron_spec* spec, int64_t first, int64_t count, 
 void validate_kron_spec(const bfs_kron_spec* spec);
 // bfs.cu
 void bfs_alloc_state(bfs_graph_s* g);
+void bfs_build_tiles(bfs_graph_s* g);
 void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* depth_out);
 void bfs_release_loop(bfs_graph_s* g);
 int64_t component_tuples_impl(bfs_graph_s* g);
