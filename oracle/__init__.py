@@ -14,6 +14,7 @@ Functions and the passage each follows:
 * ``kron_edges``              -- Graph500 Kronecker generator
 * ``build_csr``               -- CSR, each undirected edge as two arcs
 * ``degree_reindex`` / ``relabel_csr`` -- section 3.4 locality reindex
+* ``degree_reindex_local``   -- the same per partition: block partition, then local IDs
 * ``sort_rows_by_degree``     -- section 3.4 row order without relabeling
 * ``bfs``                     -- serial FIFO BFS, the plain definition
 * ``validate``                -- Graph500 validator V1-V6
@@ -71,6 +72,8 @@ def _L():
             lib.orc_build_csr.restype = i64
             lib.orc_degree_reindex.argtypes = [i64, P, i64, P, P]
             lib.orc_degree_reindex.restype = i32
+            lib.orc_degree_reindex_local.argtypes = [i64, P, i64, P, P]
+            lib.orc_degree_reindex_local.restype = i32
             lib.orc_relabel_csr.argtypes = [i64, P, P, P, P, P, P]
             lib.orc_sort_rows_by_degree.argtypes = [i64, P, P]
             lib.orc_bfs.argtypes = [i64, P, P, i64, P, P]
@@ -177,6 +180,18 @@ def degree_reindex(g: CSR, p: int = 1):
     new_label = np.zeros(g.n, np.int64)
     position = np.zeros(g.n, np.int64)
     rc = _L().orc_degree_reindex(g.n, _p(g.offsets), p, _p(new_label), _p(position))
+    if rc != 0:
+        raise ValueError("p must divide n")
+    return new_label, position
+
+
+def degree_reindex_local(g: CSR, p: int = 1):
+    """(new_label int64[n], position int64[n]): the 1D block partition first (p blocks of
+    n/p original labels), then each block numbers its own vertices by (degree desc, ID asc)
+    ("permutation of local IDs"); position = global (degree desc, ID asc) place."""
+    new_label = np.zeros(g.n, np.int64)
+    position = np.zeros(g.n, np.int64)
+    rc = _L().orc_degree_reindex_local(g.n, _p(g.offsets), p, _p(new_label), _p(position))
     if rc != 0:
         raise ValueError("p must divide n")
     return new_label, position

@@ -227,6 +227,36 @@ int orc_degree_reindex(int64_t n, const int64_t* offsets, int64_t p, int64_t* ne
     return 0;
 }
 
+/* Partition-local degree reindex ("after partitioning, a vertex is identified
+ * by ... a global ID ... and a local ID ... permutation of local IDs ... reorder
+ * vertices in memory to improve local partition access locality").  The 1D block
+ * partition comes first: partition b holds the original labels [b*per, (b+1)*per),
+ * per = n / p.  Each partition then numbers its own vertices by (degree descending,
+ * ID ascending): new label = b*per + (index of v among partition b's vertices in that
+ * order).  position[v] = v's place in the GLOBAL (degree desc, ID asc) order, which
+ * orders the rows (decreasing connectivity).  p = 1 gives orc_degree_reindex.
+ * Walking the global order once, each partition hands out its next local index. */
+int orc_degree_reindex_local(int64_t n, const int64_t* offsets, int64_t p, int64_t* new_label, int64_t* position) {
+    if (p <= 0 || n % p != 0) return -1;
+    int64_t* order = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int64_t* deg = (int64_t*)malloc((size_t)(n > 0 ? n : 1) * sizeof(int64_t));
+    int64_t* next = (int64_t*)calloc((size_t)p, sizeof(int64_t));
+    for (int64_t v = 0; v < n; ++v) { order[v] = v; deg[v] = offsets[v + 1] - offsets[v]; }
+    g_sort_deg = deg;
+    qsort(order, (size_t)n, sizeof(int64_t), cmp_deg_desc_id_asc);
+    int64_t per = n / p;
+    for (int64_t k = 0; k < n; ++k) {
+        int64_t v = order[k];
+        int64_t b = v / per;
+        position[v] = k;
+        new_label[v] = b * per + next[b]++;
+    }
+    free(next);
+    free(order);
+    free(deg);
+    return 0;
+}
+
 /* Relabel a CSR through new_label and order every row by the neighbour's
  * position (degree descending, ties by original ID: S:189).  Row of new vertex
  * new_label[v] = { new_label[x] : x in adj(v) }. */

@@ -115,6 +115,35 @@ def test_reindex_round_robin_partitions():
         assert {int(pos[v]) % 4 for v in range(n) if new[v] // 16 == part} == {part}
 
 
+@pytest.mark.parametrize("p", [1, 2, 4, 8])
+@pytest.mark.parametrize("seed", range(2))
+def test_reindex_partition_local(p, seed):
+    """P:158 'after partitioning ... permutation of local IDs': pinned by the properties that
+    determine the labelling uniquely -- a permutation that keeps every vertex in its block,
+    with degree non-increasing and, among equal degrees, original ID increasing in the new
+    label inside each block -- and by p = 1 being the global reindex."""
+    n, uv = graphs.skewed_edges(128, 900, seed)
+    g = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+    new, pos = oracle.degree_reindex_local(g, p)
+    per = n // p
+    deg = g.degree()
+    assert sorted(new.tolist()) == list(range(n))
+    assert np.array_equal(new // per, np.arange(n) // per)               # ownership preserved
+    for b in range(p):
+        members = sorted((int(new[v]), -int(deg[v]), v) for v in range(b * per, (b + 1) * per))
+        keys = [(m[1], m[2]) for m in members]                             # in new-label order
+        assert keys == sorted(keys)                                        # degree desc, then ID asc
+    gnew, gpos = oracle.degree_reindex(g, 1)
+    assert np.array_equal(pos, gpos)                                       # rows: global degree order
+    if p == 1:
+        assert np.array_equal(new, gnew)
+    r = oracle.relabel_csr(g, new, pos)
+    rdeg = r.degree()
+    assert np.array_equal(rdeg[new], deg)
+    for root in (0, int(np.argmax(deg))):                                  # S:200 levels unchanged
+        assert np.array_equal(oracle.bfs(r, int(new[root]))[0][new], oracle.bfs(g, root)[0])
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_relabel_preserves_structure(seed):
     n, uv = graphs.skewed_edges(200, 1500, seed)
