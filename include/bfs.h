@@ -233,7 +233,10 @@ bfs_status bfs_graph_destroy(bfs_graph_t g);
  * send/recv after an allgather of the p x p claim counts (Alg. 2 PushFrontiers);
  * the four switch counters are allreduced, so every rank takes the same direction.
  * Parents travel with the top-down claims, so no separate aggregation step is
- * needed (contrast P:79).
+ * needed (contrast P:79).  With reindex_by_degree the
+ * reindex is partition-local (the block partition of the original labels
+ * first, then each rank permutes its own local IDs by degree), so every rank
+ * produces the outputs of its own original labels (n must be divisible by 32*p).
  * One process per GPU: rank 0 calls bfs_comm_unique_id and ships the 128 bytes to
  * the other ranks (e.g. torch.distributed broadcast); every rank then calls
  * bfs_comm_create with its rank and CUDA device.  NCCL is loaded at run time

@@ -147,7 +147,7 @@ bfs_status bfs_graph_create(const bfs_graph_desc* desc, bfs_comm_t comm, void* c
     if (n < 1) fail(BFS_ERR_INVALID_ARG, "n must be >= 1");
     if (n > 0x7fffffffLL) fail(BFS_ERR_CAPACITY, "n = " + std::to_string(n) + " exceeds int32 vertex IDs");
     if (d.opts.reindex_by_degree && comm && comm->nranks > 1 && n % (32 * (int64_t)comm->nranks) != 0)
-        fail(BFS_ERR_INVALID_ARG, "reindex_by_degree on p ranks deals degree ranks round-robin and needs n "
+        fail(BFS_ERR_INVALID_ARG, "reindex_by_degree on p ranks permutes equal word-aligned blocks and needs n "
                                   "divisible by 32*p");
     if (d.opts.reindex_by_degree && d.kind == BFS_SRC_CSR)
         fail(BFS_ERR_INVALID_ARG, "reindex_by_degree needs an EDGES or KRONECKER source");

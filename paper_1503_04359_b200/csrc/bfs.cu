@@ -980,51 +980,12 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     }
     const int ntimed = lt ? (int)std::min<size_t>(g->levels.size(), kMaxTimed) : 0;
     if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
-    const bool aggregate = (od || op) && g->reindexed && mg;
-    if (aggregate) {
-        // final aggregation: records to the owners of the original labels
-        BFS_CUDA(cudaEventRecord(g->ev[3], s));
-        unsigned long long* dc = (unsigned long long*)g->out_cnt.p;   // [p] per-destination counts / cursors
-        BFS_CUDA(cudaMemsetAsync(dc, 0, (size_t)p * 8, s));
-        const int agrid = grid_for(nl, 256);
-        k_agg_records<<<agrid, 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->ilabel.p, nl, g->lo, root_l, g->nb, p, dc,
-                                            nullptr);
+    if ((od || op) && g->reindexed && mg) {
+        // partition-local reindex: every owned output is produced on this rank
+        k_emit_local<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->lo, nl, root_l, od,
+                                                       op);
         BFS_CHECK_LAUNCH();
-        BFS_CUDA(cudaMemcpyAsync(g->cnt_mat.p + (size_t)me * p, dc, (size_t)p * 8, cudaMemcpyDeviceToDevice, s));
-        g->comm->allgather_inplace(g->cnt_mat.p, (size_t)p * 8, s);
-        BFS_CUDA(cudaMemcpyAsync(g->h_cnt_mat, g->cnt_mat.p, (size_t)p * p * 8, cudaMemcpyDeviceToHost, s));
-        BFS_CUDA(cudaStreamSynchronize(s));
-        std::vector<int64_t> soff(p + 1, 0);
-        for (int q = 0; q < p; ++q) soff[q + 1] = soff[q] + g->h_cnt_mat[(size_t)me * p + q];
-        int64_t R = 0;
-        for (int q = 0; q < p; ++q) R += q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
-        ensure(g->agg_send, (size_t)std::max<int64_t>(soff[p], 1), s);
-        ensure(g->agg_recv, (size_t)std::max<int64_t>(R, 1), s);
-        BFS_CUDA(cudaMemcpyAsync(dc, soff.data(), (size_t)p * 8, cudaMemcpyHostToDevice, s));
-        k_agg_records<<<agrid, 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->ilabel.p, nl, g->lo, root_l, g->nb, p, dc,
-                                            g->agg_send.p);
-        BFS_CHECK_LAUNCH();
-        int64_t roff = 0;
-        uint64_t nvl_agg = 0;
-        for (int q = 0; q < p; ++q) {
-            const int64_t in_q = q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
-            sendp[q] = g->agg_send.p + soff[q];
-            sendb[q] = q == me ? 0 : (size_t)(soff[q + 1] - soff[q]) * sizeof(int4);
-            recvp[q] = g->agg_recv.p + roff;
-            recvb[q] = (size_t)in_q * sizeof(int4);
-            roff += in_q;
-            nvl_agg += sendb[q];
-        }
-        g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
-        if (od) BFS_CUDA(cudaMemsetAsync(od, 0xff, (size_t)nl * 4, s));   // -1: unreached
-        if (op) BFS_CUDA(cudaMemsetAsync(op, 0xff, (size_t)nl * 4, s));
-        const int64_t mine = soff[me + 1] - soff[me];
-        if (mine)
-            k_agg_scatter<<<grid_for(mine, 256), 256, 0, s>>>(g->agg_send.p + soff[me], mine, g->lo, od, op);
-        if (R) k_agg_scatter<<<grid_for(R, 256), 256, 0, s>>>(g->agg_recv.p, R, g->lo, od, op);
-        BFS_CHECK_LAUNCH();
-        launches += 2 + (mine ? 1 : 0) + (R ? 1 : 0);
-        nvl_total += nvl_agg;
+        ++launches;
     } else if (od || op) {
         if (g->reindexed) {
             k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
@@ -1075,11 +1036,6 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     g->run.ms_compute = lt ? comp : ms - ms_init;
     g->run.ms_push = push;
     g->run.ms_pull = pull;
-    if (aggregate) {
-        float ma = 0;
-        BFS_CUDA(cudaEventElapsedTime(&ma, g->ev[3], g->ev[1]));
-        g->run.ms_aggregate = ma;
-    }
     g->last_root_l = root_l;
     g->run.component_edge_tuples = -1;  // computed lazily by bfs_stats
 }

@@ -849,54 +849,20 @@ __global__ void k_mark_unreached(const uint32_t* __restrict__ visited, const uin
     }
 }
 
-// Final parent aggregation of a degree-reindexed search on p ranks (parents "collected
-// from the different address spaces in a final aggregation step"): every reached owned
-// vertex becomes an (original label, depth, parent) record for the rank that owns the
-// original label.  A block counts its records per destination in shared memory, reserves
-// one range per destination with a single atomicAdd, then writes them.
-constexpr int kAggMaxRanks = 64;
-
-__device__ __forceinline__ bool agg_reached(const uint32_t* visited, const uint32_t* skip, int64_t i, int64_t root_l) {
-    const uint32_t r = __ldg(visited + (i >> 5)) & ~__ldg(skip + (i >> 5));
-    return ((r >> (i & 31)) & 1u) || i == root_l;
-}
-
-__global__ void k_agg_records(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
-                              const int2* __restrict__ rec, const int32_t* __restrict__ ilabel, int64_t nl,
-                              int64_t lo, int64_t root_l, int64_t nb, int p, unsigned long long* __restrict__ cur,
-                              int4* __restrict__ out) {
-    __shared__ unsigned int s_cnt[kAggMaxRanks], s_pos[kAggMaxRanks];
-    __shared__ unsigned long long s_base[kAggMaxRanks];
-    const int64_t tile = blockDim.x;
-    for (int64_t t0 = blockIdx.x * tile; t0 < nl; t0 += (int64_t)gridDim.x * tile) {
-        if (threadIdx.x < p) s_cnt[threadIdx.x] = s_pos[threadIdx.x] = 0;
-        __syncthreads();
-        const int64_t i = t0 + threadIdx.x;
-        const bool r = i < nl && agg_reached(visited, skip, i, root_l);
-        const int32_t v = r ? __ldg(ilabel + lo + i) : 0;
-        const int dst = r ? (int)(v / nb) : 0;
-        if (r) atomicAdd(&s_cnt[dst], 1u);
-        __syncthreads();
-        // count pass (out == nullptr): cur accumulates the totals; write pass: cur holds
-        // the per-destination cursors (initialised to the send offsets)
-        if (threadIdx.x < p && s_cnt[threadIdx.x])
-            s_base[threadIdx.x] = atomicAdd(cur + threadIdx.x, (unsigned long long)s_cnt[threadIdx.x]);
-        __syncthreads();
-        if (out && r) {
-            const unsigned k = atomicAdd(&s_pos[dst], 1u);
-            const int2 o = rec[i];
-            out[s_base[dst] + k] = make_int4(v, o.x, o.y, 0);
-        }
-        __syncthreads();
-    }
-}
-
-__global__ void k_agg_scatter(const int4* __restrict__ in, int64_t R, int64_t lo, int32_t* __restrict__ depth,
-                              int32_t* __restrict__ parent) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < R; k += (int64_t)gridDim.x * blockDim.x) {
-        const int4 r = in[k];
-        if (depth) depth[r.x - lo] = r.y;
-        if (parent) parent[r.x - lo] = r.z;
+// Output pass of a degree-reindexed search on p ranks: the reindex is partition-local
+// (P:158), so the internal label of every owned original label is owned too and the
+// outputs need no exchange.  v runs over the owned ORIGINAL labels, iv = label[v] - lo
+// over the owned internal ones; unreached vertices get -1.
+__global__ void k_emit_local(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                             const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t lo, int64_t nl,
+                             int64_t root_l, int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t iv = (int64_t)__ldcs(label + lo + v) - lo;
+        const uint32_t r = __ldg(visited + (iv >> 5)) & ~__ldg(skip + (iv >> 5));
+        int2 o = make_int2(-1, -1);
+        if (((r >> (iv & 31)) & 1u) || iv == root_l) o = rec[iv];
+        if (depth) __stcs(depth + v, o.x);
+        if (parent) __stcs(parent + v, o.y);
     }
 }
 

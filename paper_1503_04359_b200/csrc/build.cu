@@ -169,30 +169,26 @@ __global__ void k_head_parent(const int2* head, const int32_t* ilabel, int64_t n
     }
 }
 
-// Degree reindex on p ranks (SURVEY 8(e) partitioning; the oracle's orc_degree_reindex):
-// position k of the (degree desc, ID asc) order is dealt round-robin, internal label
-// (k % p) * nb + k / p (nb = n / p), so every rank owns an equal share of the hubs and
-// its own vertices in degree order (isolated ones last).
-__global__ void k_deal(const int32_t* order, int64_t n, int p, int64_t nb, int32_t* label, int32_t* ilabel) {
-    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
-        const int32_t v = order[k];
-        const int64_t id = (k % p) * nb + k / p;
-        label[v] = (int32_t)id;
-        ilabel[id] = v;
+// Degree reindex on p ranks ("after partitioning ... permutation of local IDs";
+// the oracle's orc_degree_reindex_local): the 1D block partition of the ORIGINAL labels
+// comes first, then every block numbers its own vertices by (degree desc, ID asc).  A
+// stable sort of the global (degree desc, ID asc) order by block gives, at index i,
+// the vertex with internal label i (all blocks but the last hold exactly nb labels).
+// Ownership is unchanged, so the outputs of a rank's vertices stay on the rank.
+__global__ void k_block_keys(const int32_t* order, int64_t n, int64_t nb, uint32_t* keys) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x)
+        keys[k] = (uint32_t)(order[k] / nb);
+}
+__global__ void k_labels_of(const int32_t* sorted, int64_t n, int32_t* label, int32_t* ilabel) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        label[sorted[i]] = (int32_t)i;
+        ilabel[i] = sorted[i];
     }
 }
-// internal label <-> degree position (rows are kept in global degree order)
-__global__ void k_ids_to_pos(int32_t* adj, int64_t arcs, int p, int64_t nb) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < arcs; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t id = adj[j];
-        adj[j] = (int32_t)((id % nb) * p + id / nb);
-    }
-}
-__global__ void k_pos_to_ids(int32_t* adj, int64_t arcs, int p, int64_t nb) {
-    for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < arcs; j += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t k = adj[j];
-        adj[j] = (int32_t)((k % p) * nb + k / p);
-    }
+// out[i] = a[b[i]]
+__global__ void k_compose(const int32_t* a, const int32_t* b, int64_t n, int32_t* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[b[i]];
 }
 
 // degree-order helpers: key = maxdeg - deg (ascending key = descending degree)
@@ -797,12 +793,28 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         g->deg_raw.reset();
         const bool mg = g->comm && g->comm->nranks > 1;
         const int p = mg ? g->comm->nranks : 1;
+        DevBuf<int32_t> pos_of_id, id_of_pos;   // p ranks: internal label <-> global degree position
         if (mg) {
-            // round-robin deal of the degree positions (nb = n / p, checked by the ABI)
-            DevBuf<int32_t> lab, ilab;
+            // partition-local labels (nb = n / p, checked by the ABI): stable sort of the
+            // global degree order by block
+            DevBuf<uint32_t> keys;
+            DevBuf<int32_t> sorted, lab, ilab;
+            keys.alloc((size_t)g->n, s);
+            sorted.alloc((size_t)g->n, s);
+            BFS_CUDA(cudaMemcpyAsync(sorted.p, order.p, (size_t)g->n * 4, cudaMemcpyDeviceToDevice, s));
+            k_block_keys<<<grid_for(g->n, 256), 256, 0, s>>>(order.p, g->n, g->nb, keys.p);
+            BFS_CHECK_LAUNCH();
+            radix_sort_pairs(keys.p, sorted.p, g->n, 32 - __builtin_clz((unsigned)p), s);
+            keys.reset();
             lab.alloc((size_t)g->n, s);
             ilab.alloc((size_t)g->n, s);
-            k_deal<<<grid_for(g->n, 256), 256, 0, s>>>(order.p, g->n, p, g->nb, lab.p, ilab.p);
+            k_labels_of<<<grid_for(g->n, 256), 256, 0, s>>>(sorted.p, g->n, lab.p, ilab.p);
+            BFS_CHECK_LAUNCH();
+            sorted.reset();
+            pos_of_id.alloc((size_t)g->n, s);
+            id_of_pos.alloc((size_t)g->n, s);
+            k_compose<<<grid_for(g->n, 256), 256, 0, s>>>(rank.p, ilab.p, g->n, pos_of_id.p);
+            k_compose<<<grid_for(g->n, 256), 256, 0, s>>>(lab.p, order.p, g->n, id_of_pos.p);
             BFS_CHECK_LAUNCH();
             rank.reset();
             order.reset();
@@ -814,14 +826,14 @@ void build_graph(bfs_graph_s* g, const bfs_graph_desc* d) {
         }
         build_pass(g, d, g->label.p);
         if (mg) {
-            // rows in global degree order, not in the order of the dealt labels
-            k_ids_to_pos<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, p, g->nb);
+            // rows in global degree order, not in the order of the local labels
+            k_map_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, pos_of_id.p);
             BFS_CHECK_LAUNCH();
             const bfs_build_opts keep = g->opts;
             g->opts = bfs_build_opts{0, 0, 0, 1};
             sort_and_compact(g);
             g->opts = keep;
-            k_pos_to_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, p, g->nb);
+            k_map_ids<<<grid_for(g->arcs_local, 256), 256, 0, s>>>(g->adj.p, g->arcs_local, id_of_pos.p);
             BFS_CHECK_LAUNCH();
         }
         g->reindexed = true;

@@ -158,7 +158,6 @@ struct bfs_graph_s {
     bfsb::DevBuf<uint32_t> seen;     // [n/32] remote vertices already claimed this BFS
     bfsb::DevBuf<int2> out_list, in_list;  // (vertex, parent) claims
     bfsb::DevBuf<int32_t> flist;     // sparse pull: frontier vertices received from peers
-    bfsb::DevBuf<int4> agg_send, agg_recv;  // reindexed p ranks: final (label, depth, parent) records
     bfsb::DevBuf<int64_t> out_cnt;   // [p]
     bfsb::DevBuf<int64_t> cnt_mat;   // [p*p] claim counts, row = sender
     int64_t* h_cnt_mat = nullptr;    // pinned mirror
