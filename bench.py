@@ -227,6 +227,29 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- our arm
+def rank_memory(scale: int, ef: int, p: int, reindex: bool) -> dict:
+    """Device bytes one rank needs: n = 2^scale, nl = n/p owned
+    vertices, raw arcs per rank = 2 * ef * n / p (each tuple is two arcs).
+    steady: adjacency 4/arc + per owned vertex off 8, head 8, deg_raw 4, queues 16,
+    prefix 8, records 8 (+ hpar 4 when reindexed) + global arrays label/ilabel 8n (when
+    reindexed) + bitmaps (visited, skip: nl/8 each; front, next, seen: n/8 each) + the
+    top-down claim lists (p ranks: up to 8 bytes per owned-vertex slot of every peer,
+    8 nb p = 8n, plus the receive side) + the tile index (one GPU, reindexed: ~2.3 GB at
+    K29).  build_peak: offsets + raw degrees + two raw-arc arrays (fill target and
+    sort/compaction target), 8 bytes per raw arc."""
+    n = 1 << scale
+    nl = n // p
+    raw = 2 * ef * n // p
+    steady = 4 * raw + nl * (8 + 8 + 4 + 16 + 8 + 8 + (4 if reindex else 0)) + (8 * n if reindex else 0)
+    steady += 2 * nl // 8 + 3 * n // 8
+    if p > 1:
+        steady += 8 * n + 8 * nl
+    elif reindex:
+        steady += int(4.3e9 * (n / 2 ** 29))   # tile index + record log, measured at K29
+    peak = 8 * raw + 12 * nl + (8 * n if reindex else 0)
+    return {"steady_gb": round(steady / 1e9, 1), "build_peak_gb": round(max(steady, peak) / 1e9, 1)}
+
+
 def bu_bytes(n_bits: int, lv: dict) -> int:
     """Algorithmic bytes of one bottom-up launch, SURVEY section 8(d) exactly: visited
     scan, frontier and next bitmaps over the n_bits vertices the step covers (3 n/8;
@@ -306,6 +329,11 @@ def main():
         torch.cuda.synchronize()
 
     cfg = CONFIGS[args.config]
+    mem = rank_memory(cfg["scale"], cfg["ef"], ws, bool(args.reindex))
+    total = torch.cuda.mem_get_info()[1]
+    if mem["build_peak_gb"] * 1e9 > total:
+        raise SystemExit(f"{args.config} on {ws} GPU(s) needs ~{mem['build_peak_gb']} GB per rank "
+                         f"(DESIGN.md section 7), the device has {total / 1e9:.0f} GB: use more GPUs")
     stream = torch.cuda.Stream()
     opts = pkg.default_opts(reindex_by_degree=bool(args.reindex), sort_rows=2 if args.rows == "degree" else 1)
     g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"], opts=opts, comm=comm, stream=stream)
@@ -447,7 +475,7 @@ def main():
                    "beta": args.paper_beta if args.policy == "paper" else args.beta, "parallelism": f"1d{ws}",
                    "reindex_by_degree": bool(args.reindex), "row_order": args.rows,
                    "l2": "inputs larger than L2 (CSR %.1f GB vs 126 MB L2)" % ((8 * (n + 1) + 4 * g.arcs) / 1e9)},
-        "build_ms": round(build_ms, 2), "arcs": g.arcs,
+        "build_ms": round(build_ms, 2), "arcs": g.arcs, "rank_memory_model": mem,
         "per_root_ms": {"min": round(min(times), 4), "median": round(statistics.median(times), 4),
                         "max": round(max(times), 4)},
         "gteps_min_median_max": [round(min(rates), 3), round(statistics.median(rates), 3), round(max(rates), 3)],

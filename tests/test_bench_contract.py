@@ -46,3 +46,18 @@ def test_our_arm_line_k16():
     assert "sm_mhz" in d["clocks"]
     v = d["validation"]
     assert v["searches"] == 64 and v["failed_searches"] == 0 and v["rules"] == {}
+
+
+def test_rank_memory_model_fits_the_multi_gpu_targets():
+    """K29 fits one B200 (178 GB usable), K30 needs >= 2 ranks, and
+    the 8-rank targets (K29, K30) fit with room for the construction peak."""
+    import bench
+    gb = 178.0
+    assert bench.rank_memory(29, 16, 1, True)["build_peak_gb"] < gb
+    assert bench.rank_memory(30, 16, 1, True)["steady_gb"] > gb
+    for scale in (29, 30):
+        m = bench.rank_memory(scale, 16, 8, True)
+        assert m["build_peak_gb"] < gb / 3
+    # per-rank bytes shrink with p
+    ms = [bench.rank_memory(30, 16, p, True)["steady_gb"] for p in (2, 4, 8)]
+    assert ms == sorted(ms, reverse=True)
