@@ -97,6 +97,9 @@ static int64_t env_i64(const char* name, int64_t dflt) {
 }
 // top-down steps with at least this many arcs run tiled when the graph has a tile index
 static int64_t tile_min_setting() { return env_i64("BFS_TILE_MIN", (int64_t)1 << 24); }
+// top-down steps with at most this many arcs run as one kernel on the device loop
+// (k_td_small; BFS_TD_SMALL=-1 disables it)
+static int64_t td_small_setting() { return env_i64("BFS_TD_SMALL", (int64_t)1 << 15); }
 
 TileLog tile_log(const bfs_graph_s* g) {
     return TileLog{g->tile_pool.p, g->tile_ubase.p, g->tile_ucnt.p, g->tile_lpool.p, g->tile_lcnt.p,
@@ -393,22 +396,33 @@ static void build_loop_graph(bfs_graph_s* g) {
 
     cudaGraph_t G;
     BFS_CUDA(cudaGraphCreate(&G, 0));
-    cudaGraphConditionalHandle h_loop, h_td, h_bu;
+    cudaGraphConditionalHandle h_loop, h_tds, h_td, h_bu, h_conv;
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_loop, G, 1, cudaGraphCondAssignDefault));
-    cudaGraphNode_t n_while, n_td, n_bu;
+    cudaGraphNode_t n_while, n_tds, n_td, n_bu, n_conv;
     cudaGraph_t B = add_cond(G, {}, h_loop, cudaGraphCondTypeWhile, &n_while);
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_tds, B, 0, cudaGraphCondAssignDefault));
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_td, B, 0, cudaGraphCondAssignDefault));
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_bu, B, 0, cudaGraphCondAssignDefault));
-    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step_begin, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_td, h_bu);
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_conv, B, 0, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step_begin, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_tds, h_td, h_bu,
+                                         h_conv);
+    cudaGraph_t S = add_cond(B, {n_begin}, h_tds, cudaGraphCondTypeIf, &n_tds);
     cudaGraph_t T = add_cond(B, {n_begin}, h_td, cudaGraphCondTypeIf, &n_td);
-    cudaGraph_t U = add_cond(B, {n_begin}, h_bu, cudaGraphCondTypeIf, &n_bu);
-    add_kernel(B, {n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
+    cudaGraph_t C = add_cond(B, {n_begin}, h_conv, cudaGraphCondTypeIf, &n_conv);   // BU from a queue
+    cudaGraph_t U = add_cond(B, {n_conv}, h_bu, cudaGraphCondTypeIf, &n_bu);
+    add_kernel(B, {n_tds, n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
+    // small top-down step: one kernel
+    add_kernel(S, {}, k_td_small, dim3(sms * 4), t256, 0, (const Ctl*)ctl, qa, qb, (const uint32_t*)g->front.p,
+               (const uint32_t*)g->next.p, words, (const int64_t*)g->off.p, (const int32_t*)g->adj.p,
+               (const int2*)g->head.p, g->visited.p, g->rec.p, pmap, cnt, lrec);
     // top-down body
     unsigned* hcnt = g->tile_T ? g->tile_hcnt.p : nullptr;
     const TileLog lg = tile_log(g);
+    cudaGraphConditionalHandle h_tile{};
+    if (g->tile_T) BFS_CUDA(cudaGraphConditionalHandleCreate(&h_tile, T, 0, cudaGraphCondAssignDefault));
     cudaGraphNode_t t1 = add_kernel(T, {}, k_td_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words, g->head.p, qa, qb,
                                     cnt, tstate, g->tctr.p, (const uint32_t*)g->visited.p, hcnt, g->tile_lcnt.p,
-                                    (int64_t)g->tile_nwl);
+                                    (int64_t)g->tile_nwl, h_tile, g->tile_T ? 1 : 0);
     cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, (int64_t)0, g->prefix.p,
                                     tstate, g->tctr.p, g->tile_nh, g->tile_hlist.p, hcnt, 0);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
@@ -417,15 +431,18 @@ static void build_loop_graph(bfs_graph_s* g) {
                                     qa, g->prefix.p, g->scratch64.p, (int64_t)0, (int64_t)0, g->off.p, g->adj.p,
                                     g->visited.p, g->rec.p, pmap, qb, g->head.p, cnt, (int32_t)0, g->lo, g->hi, Remote{},
                                     ctl, lrec, -1, lg);
-    if (g->tile_T) {   // heavy frontier rows and the records of a tile-mode step (return at once otherwise)
-        t4 = add_kernel(T, {t4}, k_td_tile, dim3(g->tile_units), dim3(kTileThreads), (size_t)g->tile_maxw * 4,
+    if (g->tile_T) {   // heavy frontier rows and the records of a tile-mode step (IF node set by k_td_prep)
+        cudaGraphNode_t n_tile;
+        cudaGraph_t TT = add_cond(T, {t4}, h_tile, cudaGraphCondTypeIf, &n_tile);
+        cudaGraphNode_t t5 = add_kernel(TT, {}, k_td_tile, dim3(g->tile_units), dim3(kTileThreads), (size_t)g->tile_maxw * 4,
                         (const Ctl*)ctl, (const int32_t*)g->tile_start.p, g->tile_T, (const int2*)g->tile_unit.p,
                         (const int32_t*)g->tile_bnd.p, (const int32_t*)g->tile_hlist.p, (const unsigned*)hcnt,
                         (const int64_t*)g->off.p, (const int32_t*)g->adj.p, g->visited.p, pmap, lg, lrec);
-        t4 = add_kernel(T, {t4}, k_tile_rec, dim3(g->tile_nwl), dim3(kWinThreads), (size_t)kWin * 4, (const Ctl*)ctl,
+        add_kernel(TT, {t5}, k_tile_rec, dim3(g->tile_nwl), dim3(kWinThreads), (size_t)kWin * 4, (const Ctl*)ctl,
                         (int32_t)0, (const int2*)g->tile_wl.p, (const int32_t*)g->tile_fu.p,
                         (const int2*)g->tile_unit.p, lg, (const uint32_t*)g->visited.p, (const uint32_t*)g->front.p,
                         (const uint32_t*)g->next.p, g->rec.p, lrec);
+        t4 = n_tile;
     }
     const int64_t nbatches = (words + 31) / 32;
     const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
@@ -433,9 +450,10 @@ static void build_loop_graph(bfs_graph_s* g) {
     add_kernel(T, {t4}, k_td_finish_dev, g8, t256, 0, ctl, (const uint32_t*)g->visited.p, g->front.p, g->next.p, words,
                g->head.p, qa, qb, cnt);
     // bottom-up body
-    cudaGraphNode_t u1 = add_kernel(U, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
-    cudaGraphNode_t u2 = add_kernel(U, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
-    add_kernel(U, {u2}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
+    // queue -> bitmap before a bottom-up step that follows a top-down one (IF node)
+    cudaGraphNode_t u1 = add_kernel(C, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
+    add_kernel(C, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
+    add_kernel(U, {}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
                g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
                cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
     BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
@@ -517,7 +535,8 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
                                                  g->rec.p, qa, g->head.p, (unsigned long long*)g->cnt.p, ctl, g->policy,
                                                  g->n, g->arcs_global, kGraphMaxLevels, td_claim_min(),
-                                                 (persistent || !g->tile_T) ? (int64_t)-1 : tile_min_setting());
+                                                 (persistent || !g->tile_T) ? (int64_t)-1 : tile_min_setting(),
+                                                 td_small_setting());
     BFS_CHECK_LAUNCH();
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
     if (persistent) {
@@ -595,6 +614,15 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         BFS_CUDA(cudaStreamSynchronize(s));
     }
     const LevelRec* R = reinterpret_cast<const LevelRec*>(g->h_lrec);
+    // kernels the loop graph launched for step d (between k_step_begin and k_step_end)
+    const int64_t tmin = g->tile_T ? tile_min_setting() : INT64_MAX, tsmall = td_small_setting(), cmin = td_claim_min();
+    auto small = [&](int d) { return R[d].m_f <= tsmall && R[d].m_f <= 64 * R[d].n_f; };
+    auto claimed = [&](int d) { return R[d].dir == 0 && !small(d) && (R[d].m_f >= cmin || R[d].m_f >= tmin); };
+    auto step_kernels = [&](int d) -> int64_t {
+        if (R[d].dir == 0) return small(d) ? 1 : 5 + (R[d].m_f >= tmin ? 2 : 0);
+        const bool conv = d == 0 || (R[d - 1].dir == 0 && !claimed(d - 1));   // queue -> bitmap first
+        return 1 + (conv ? 2 : 0);
+    };
     double comp = 0;
     for (int d = 0; d < c.d; ++d) {
         bfs_level_stats L{};
@@ -612,7 +640,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             comp += L.kernel_ms;
         }
         g->levels.push_back(L);
-        launches += persistent ? 0 : 2 + (R[d].dir == 0 ? 5 + (g->tile_T ? 2 : 0) : 3);
+        launches += persistent ? 0 : 2 + step_kernels(d);
     }
     float ms = 0, ms_init = 0, ms_loop = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));

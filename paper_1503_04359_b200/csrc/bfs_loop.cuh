@@ -18,7 +18,7 @@ __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __res
                            int64_t root, const int32_t* __restrict__ label, int2* __restrict__ out, Queue q,
                            const int2* __restrict__ head, unsigned long long* __restrict__ cnt, Ctl* ctl,
                            bfs_policy pol, int64_t n, int64_t arcs, int max_levels, int64_t claim_min,
-                           int64_t tile_min) {
+                           int64_t tile_min, int64_t td_small) {
     const int64_t ri = label ? (int64_t)__ldg(label + root) : root;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = skip[w];
@@ -44,6 +44,7 @@ __global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __res
         c.max_levels = max_levels;
         c.claim_min = claim_min;
         c.tile_min = tile_min;
+        c.td_small = td_small;
         *ctl = c;
     }
 }
@@ -110,15 +111,19 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
     return cont;
 }
 
-__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_td,
-                             cudaGraphConditionalHandle h_bu) {
+__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_tds,
+                             cudaGraphConditionalHandle h_td, cudaGraphConditionalHandle h_bu,
+                             cudaGraphConditionalHandle h_conv) {
     Ctl c = *ctl;
     const long long t = gtimer();
     const long long m_u = step_decide(c);
     c.E = c.m_f;
     c.nchunks = (c.E + kTdChunk - 1) / kTdChunk;
-    c.tile = c.dir == 0 && c.tile_min >= 0 && c.E >= c.tile_min;
-    c.claim = c.dir == 0 && (c.E >= c.claim_min || c.tile);
+    // k_td_small (neither claim-only nor tiled): few arcs, and no hub among the frontier
+    // vertices on average (a long row is one warp's work there)
+    const bool small = c.dir == 0 && c.E <= c.td_small && c.E <= 64 * c.n_f;
+    c.tile = c.dir == 0 && !small && c.tile_min >= 0 && c.E >= c.tile_min;
+    c.claim = c.dir == 0 && !small && (c.E >= c.claim_min || c.tile);
     LevelRec r{};
     r.n_f = c.n_f;
     r.m_f = c.m_f;
@@ -129,8 +134,90 @@ __global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, 
     lrec[c.d] = r;
     for (int i = 0; i < 8; ++i) cnt[i] = 0;
     *ctl = c;
-    cudaGraphSetConditional(h_td, c.dir == 0 ? 1u : 0u);
+    cudaGraphSetConditional(h_tds, small ? 1u : 0u);
+    cudaGraphSetConditional(h_td, (c.dir == 0 && !small) ? 1u : 0u);
     cudaGraphSetConditional(h_bu, c.dir == 1 ? 1u : 0u);
+    cudaGraphSetConditional(h_conv, (c.dir == 1 && c.have_queue && !c.front_ok) ? 1u : 0u);
+}
+
+// A small top-down step (m_f <= td_small arcs and at most 64 per frontier vertex: the
+// first levels from a low-degree root and the last levels of a search) as ONE kernel instead of the prologue / scan /
+// chunk / expand / finish chain: warp per frontier vertex, lanes over its arcs,
+// claims by atomicOr on the visited word, winners record (depth, parent) and append
+// to the next queue (one atomic per warp instruction).  The frontier is the queue or,
+// after a bottom-up step, the bitmap (its set bits are expanded in place: no b2q).
+__global__ void k_td_small(const Ctl* ctl, Queue qa, Queue qb, const uint32_t* __restrict__ f0,
+                           const uint32_t* __restrict__ f1, int64_t words, const int64_t* __restrict__ off,
+                           const int32_t* __restrict__ adj, const int2* __restrict__ head, uint32_t* __restrict__ visited,
+                           int2* __restrict__ rec, const int32_t* __restrict__ pmap, unsigned long long* __restrict__ cnt,
+                           LevelRec* lrec) {
+    const Ctl& c = *ctl;
+    if (c.dir != 0 || c.E > c.td_small || c.E > 64 * c.n_f) return;
+    stamp_begin(lrec, ctl);
+    const int lane = threadIdx.x & 31;
+    const int32_t level = c.d + 1;
+    const Queue qn = c.qsel ? qa : qb;
+    unsigned long long my_mf = 0;
+    constexpr int kU = 4;   // 32-arc groups of a row in flight per warp
+    auto expand = [&](int32_t u) {   // warp-uniform u
+        const int64_t jb = __ldg(off + u), je = __ldg(off + u + 1);
+        const int32_t par = pmap ? __ldg(pmap + u) : u;
+        for (int64_t j0 = jb; j0 < je; j0 += 32 * kU) {
+            int32_t v[kU];
+            uint32_t w[kU];
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                const int64_t j = j0 + q * 32 + lane;
+                v[q] = j < je ? __ldg(adj + j) : -1;
+            }
+#pragma unroll
+            for (int q = 0; q < kU; ++q) w[q] = v[q] >= 0 ? __ldcg(visited + (v[q] >> 5)) : kFull;
+#pragma unroll
+            for (int q = 0; q < kU; ++q) {
+                const uint32_t bit = v[q] >= 0 ? 1u << (v[q] & 31) : 0u;
+                const bool win = v[q] >= 0 && !(w[q] & bit) && !(atomicOr(visited + (v[q] >> 5), bit) & bit);
+                const unsigned m = __ballot_sync(kFull, win);
+                if (!m) continue;
+                unsigned long long base = 0;
+                if (lane == __ffs(m) - 1) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+                base = __shfl_sync(kFull, base, __ffs(m) - 1);
+                if (win) {
+                    const int32_t dg = __ldg(head + v[q]).y;
+                    rec[v[q]] = make_int2(level, par);
+                    queue_put(qn, base + __popc(m & lanemask_lt()), v[q], dg);
+                    my_mf += (unsigned long long)dg;
+                }
+            }
+        }
+    };
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if (c.have_queue) {
+        const int32_t* qv = c.qsel ? qb.v : qa.v;
+        for (int64_t i = gw; i < c.n_f; i += nw) expand(__ldg(qv + i));
+    } else {
+        const uint32_t* fr = c.fsel ? f1 : f0;
+        for (int64_t b0 = gw * 32; b0 < words; b0 += nw * 32) {
+            const uint32_t x = b0 + lane < words ? __ldcg(fr + b0 + lane) : 0u;
+            unsigned todo = __ballot_sync(kFull, x != 0u);
+            while (todo) {
+                const int q = __ffs(todo) - 1;
+                todo &= todo - 1;
+                uint32_t bits = __shfl_sync(kFull, x, q);
+                while (bits) {
+                    const int k = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    expand((int32_t)((b0 + q) * 32 + k));
+                }
+            }
+        }
+    }
+    my_mf = warp_sum_u64(my_mf);
+    if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+    if (lrec) {
+        __syncthreads();
+        stamp_end(lrec, ctl);
+    }
 }
 
 __global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* cnt, cudaGraphConditionalHandle h_loop) {
@@ -146,13 +233,15 @@ __global__ void k_td_prep(const Ctl* ctl, uint32_t* __restrict__ f0, uint32_t* _
                           int64_t words, const int2* __restrict__ head, Queue qa, Queue qb,
                           unsigned long long* __restrict__ cnt, unsigned long long* __restrict__ tstate,
                           unsigned int* __restrict__ tctr, const uint32_t* __restrict__ visited,
-                          unsigned* __restrict__ hcount, unsigned* __restrict__ lcnt, int64_t nwl) {
+                          unsigned* __restrict__ hcount, unsigned* __restrict__ lcnt, int64_t nwl,
+                          cudaGraphConditionalHandle h_tile, int has_tile) {
     const int64_t tiles = (ctl->n_f + 2047) / 2048;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tiles; i += (int64_t)gridDim.x * blockDim.x)
         tstate[i] = 0ull;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         *tctr = 0u;
         if (hcount) *hcount = 0u;   // heavy list (tile mode)
+        if (has_tile) cudaGraphSetConditional(h_tile, ctl->tile ? 1u : 0u);
     }
     if (ctl->tile && lcnt)   // light-row record buckets (tile mode)
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nwl; i += (int64_t)gridDim.x * blockDim.x)

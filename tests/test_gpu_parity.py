@@ -379,6 +379,7 @@ def test_claim_only_topdown_steps(loop, monkeypatch):
     """Large top-down steps run claim-only + k_td_finish (winners read back in vertex order).
     Forcing it on every top-down step (BFS_TD_CLAIM_MIN=1) must change nothing observable."""
     monkeypatch.setenv("BFS_TD_CLAIM_MIN", "1")
+    monkeypatch.setenv("BFS_TD_SMALL", "-1")   # small steps would take the one-kernel path
     for name in ("g1", "union", "skewed", "random", "grid"):
         n, uv = FIXTURES[name]
         g = pkg.Graph.from_edges(uv, n)
@@ -392,6 +393,29 @@ def test_claim_only_topdown_steps(loop, monkeypatch):
     for r in g.sample_roots(14, 9, 4):
         _check_outputs(g, ref, int(r), dict(loop=loop, mode=1))
         _check_outputs(g, ref, int(r), dict(loop=loop, mode=0, alpha=30, beta=1000))
+    g.close()
+
+
+@pytest.mark.parametrize("small", ["-1", str(1 << 40)])
+def test_small_topdown_kernel(small, monkeypatch):
+    """Top-down steps with m_f <= BFS_TD_SMALL run as one kernel on the device loop
+    (k_td_small: warp per frontier vertex, from the queue or straight from the bitmap
+    after a bottom-up step).  Forcing it on every top-down step, hub roots included, and
+    disabling it must both leave every output and counter exact."""
+    monkeypatch.setenv("BFS_TD_SMALL", small)
+    for name in ("g1", "union", "skewed", "grid"):
+        n, uv = FIXTURES[name]
+        g = pkg.Graph.from_edges(uv, n)
+        ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+        for root in sorted({0, n - 1, int(np.argmax(ref.degree()))}):
+            for pol in (dict(mode=0), dict(mode=1), dict(mode=3, alpha=500, beta=2), dict(mode=2, bu_from_level=1)):
+                _check_run(g, ref, root, dict(loop="graph", **pol), uv)
+        g.close()
+    uv, ref = oracle.kron_graph(14, 16, 9)
+    g = pkg.Graph.kronecker(14, 16, 9, opts=pkg.default_opts(reindex_by_degree=True))
+    for r in list(g.sample_roots(14, 9, 3)) + [int(np.argmax(ref.degree()))]:
+        _check_outputs(g, ref, int(r), dict(loop="graph", mode=1))
+        _check_outputs(g, ref, int(r), dict(loop="graph", mode=0, alpha=30, beta=1000))
     g.close()
 
 

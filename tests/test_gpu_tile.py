@@ -40,6 +40,7 @@ def test_tile_mode_parity(monkeypatch, knobs, scale, abc, seed):
     for k, v in knobs.items():
         monkeypatch.setenv(k, v)
     monkeypatch.setenv("BFS_TILE_MIN", "1")
+    monkeypatch.setenv("BFS_TD_SMALL", "-1")   # no step takes the one-kernel small path
     g = pkg.Graph.kronecker(scale, 16, seed, abc, opts=pkg.default_opts(**REIDX))
     info = pkg.bfs_graph_tiles(g.h)
     assert info["tiles"] > 0 and info["heavy_rows"] > 0, info
@@ -72,6 +73,7 @@ def test_tile_mode_hub_root_k16(monkeypatch):
     """default tile sizes, heavy threshold lowered: the first top-down steps from a hub"""
     monkeypatch.setenv("BFS_TILE_H", "256")
     monkeypatch.setenv("BFS_TILE_MIN", "1024")
+    monkeypatch.setenv("BFS_TD_SMALL", "-1")
     g = pkg.Graph.kronecker(16, 16, 1, oracle.KRON_ABC, opts=pkg.default_opts(**REIDX))
     assert pkg.bfs_graph_tiles(g.h)["tiles"] > 0
     uv, ref = oracle.kron_graph(16, 16, 1, oracle.KRON_ABC)
