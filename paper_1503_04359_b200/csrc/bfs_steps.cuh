@@ -385,7 +385,7 @@ constexpr int kBuWarps = 8;
 constexpr int kBuCtas = 4;     // resident CTAs per SM (launch bound and grid; 5 spills: -10%)
 constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 8;
-constexpr int kBuVec = 4;      // arcs a slot reads (one aligned vector load) and probes per round
+constexpr int kBuVec = 4;      // arcs a slot reads (aligned vector loads: 2, 4 or 8) and probes per round
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
 __global__ void __launch_bounds__(kBuWarps * 32, kBuCtas)
@@ -576,7 +576,12 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
 #pragma unroll
                 for (int s = 0; s < kBuSlots; ++s) {
                     const int64_t b = sj[s] & ~(int64_t)(kBuVec - 1);
-                    if (kBuVec == 4) {
+                    if (kBuVec == 8) {   // one whole 32-byte sector
+                        const int4 x = sa[s] ? __ldg(reinterpret_cast<const int4*>(adj + b)) : make_int4(0, 0, 0, 0);
+                        const int4 y = sa[s] ? __ldg(reinterpret_cast<const int4*>(adj + b) + 1) : make_int4(0, 0, 0, 0);
+                        a[s][0] = x.x; a[s][1] = x.y; a[s][2 % kBuVec] = x.z; a[s][3 % kBuVec] = x.w;
+                        a[s][4 % kBuVec] = y.x; a[s][5 % kBuVec] = y.y; a[s][6 % kBuVec] = y.z; a[s][7 % kBuVec] = y.w;
+                    } else if (kBuVec == 4) {
                         const int4 x = sa[s] ? __ldg(reinterpret_cast<const int4*>(adj + b)) : make_int4(0, 0, 0, 0);
                         a[s][0] = x.x; a[s][1] = x.y; a[s][2 % kBuVec] = x.z; a[s][3 % kBuVec] = x.w;
                     } else if (kBuVec == 2) {
