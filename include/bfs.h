@@ -94,8 +94,10 @@ typedef struct {
  *   the persistent one-kernel search for graphs up to 2^22 arcs, the CUDA loop graph
  *   (conditional WHILE/IF nodes) above; on p ranks the host (the exchange sizes are
  *   host decisions).  1 = host-driven loop (one synchronisation per level).  2 = the
- *   loop graph, 3 = the persistent kernel (one GPU; else host).  All give identical
- *   outputs and statistics (one host synchronisation per search on the device loops).
+ *   loop graph, 3 = the persistent kernel (one GPU; else host), 4 = the persistent
+ *   search as ONE thread-block cluster (up to 16 CTAs; levels separated by the
+ *   hardware cluster barrier; one GPU).  All give identical outputs and statistics
+ *   (one host synchronisation per search on the device loops).
  * Defaults: mode 0, alpha 15, beta 18, bu_from_level 0, level_times 0, loop 0. */
 typedef struct {
     int mode;

@@ -211,12 +211,12 @@ def bfs_graph_build_ms(h) -> float:
     return x.value
 
 
-LOOPS = {"auto": 0, "host": 1, "graph": 2, "persistent": 3}
+LOOPS = {"auto": 0, "host": 1, "graph": 2, "persistent": 3, "cluster": 4}
 
 
 def bfs_set_policy(h, mode: int = 0, alpha: int = 15, beta: int = 18, bu_from_level: int = 0, level_times: bool = False,
                    loop="auto", host_loop: bool = False):
-    """loop: 'auto' | 'host' | 'graph' | 'persistent' (or 0..3); host_loop=True is loop='host'."""
+    """loop: 'auto' | 'host' | 'graph' | 'persistent' | 'cluster' (or 0..4); host_loop=True is loop='host'."""
     lp = 1 if host_loop else (LOOPS[loop] if isinstance(loop, str) else int(loop))
     p = bfs_policy(mode, alpha, beta, bu_from_level, int(level_times), lp)
     _check(lib().bfs_set_policy(h, ctypes.byref(p)))

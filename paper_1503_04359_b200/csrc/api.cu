@@ -305,7 +305,8 @@ bfs_status bfs_set_policy(bfs_graph_t g, const bfs_policy* p) {
     if (p->alpha < 1 || p->alpha > (1 << 24) || p->beta < 1 || p->beta > (1 << 24))
         fail(BFS_ERR_INVALID_ARG, "alpha and beta must be in [1, 2^24]");
     if (p->bu_from_level < 0) fail(BFS_ERR_INVALID_ARG, "bu_from_level must be >= 0");
-    if (p->loop < 0 || p->loop > 3) fail(BFS_ERR_INVALID_ARG, "loop must be 0 (auto), 1 (host), 2 (graph) or 3 (persistent)");
+    if (p->loop < 0 || p->loop > 4)
+        fail(BFS_ERR_INVALID_ARG, "loop must be 0 (auto), 1 (host), 2 (graph), 3 (persistent) or 4 (cluster)");
     g->policy = *p;
     API_END
 }

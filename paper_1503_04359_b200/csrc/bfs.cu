@@ -488,7 +488,8 @@ static int pers_grid() {
     if (const char* e = getenv("BFS_PERSIST_GRID")) return std::max(1, atoi(e));
     static const int gsz = [] {
         int per = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bfs_persistent, kPersThreads, 0) != cudaSuccess ||
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bfs_persistent<GridBar, kPersThreads>, kPersThreads,
+                                                          0) != cudaSuccess ||
             per < 1) {
             cudaGetLastError();
             per = 1;
@@ -502,8 +503,17 @@ static int pers_grid() {
 // One search with the device-driven loop: the loop graph, or (persistent) the
 // one-kernel search.  Returns false (nothing to report) if the search ran past
 // kGraphMaxLevels levels; the caller reruns it host-driven.
+// CTAs of the one-cluster search (BFS_CLUSTER: tuning; 16 needs the non-portable
+// cluster size, 8 is portable)
+static int cluster_size() {
+    const char* e = getenv("BFS_CLUSTER");
+    return e ? std::max(1, std::min(16, atoi(e))) : 16;
+}
+constexpr int kClusterThreads = 1024;
+
 static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op, int32_t* parent_out,
-                          int32_t* depth_out, bool persistent) {
+                          int32_t* depth_out, int mode) {
+    bool persistent = mode != 0;   // 1: one resident wave (grid barrier), 2: one thread-block cluster
     cudaStream_t s = g->stream;
     const int64_t nl = g->nl();
     if (persistent) {
@@ -564,12 +574,33 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_bfs_persistent, (const int64_t*)g->off.p,
-                                                 (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p,
-                                                 g->front.p, g->next.p, words, g->rec.p, pmap, hpar, qa, qb,
-                                                 (unsigned long long*)g->pcnt.p, g->big.p, ctl, lrec,
-                                                 GridBar{bar, bar + 1});
-        if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources) {
+        cudaError_t e;
+        if (mode == 2) {
+            // one cluster: hardware barrier.cluster between phases, guaranteed co-scheduled
+            static const bool attr_ok = [] {
+                const bool ok = cudaFuncSetAttribute(k_bfs_persistent<ClusterBar, kClusterThreads>,
+                                                     cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess;
+                cudaGetLastError();
+                return ok;
+            }();
+            cfg.gridDim = dim3(attr_ok ? cluster_size() : std::min(8, cluster_size()));
+            cfg.blockDim = dim3(kClusterThreads);
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = cfg.gridDim.x;
+            attr[0].val.clusterDim.y = 1;
+            attr[0].val.clusterDim.z = 1;
+            e = cudaLaunchKernelEx(&cfg, k_bfs_persistent<ClusterBar, kClusterThreads>, (const int64_t*)g->off.p,
+                                   (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p, g->front.p,
+                                   g->next.p, words, g->rec.p, pmap, hpar, qa, qb, (unsigned long long*)g->pcnt.p,
+                                   g->big.p, ctl, lrec, ClusterBar{});
+        } else {
+            e = cudaLaunchKernelEx(&cfg, k_bfs_persistent<GridBar, kPersThreads>, (const int64_t*)g->off.p,
+                                   (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p, g->front.p,
+                                   g->next.p, words, g->rec.p, pmap, hpar, qa, qb, (unsigned long long*)g->pcnt.p,
+                                   g->big.p, ctl, lrec, GridBar{bar, bar + 1});
+        }
+        if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources ||
+            e == cudaErrorInvalidClusterSize) {
             // the persistent grid cannot be co-resident now: the loop graph runs the
             // same steps from the state k_init_dev wrote
             cudaGetLastError();
@@ -693,12 +724,12 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         return e && e[0] == '1';
     }();
     // level loop: 0 auto (persistent kernel for small graphs, loop graph otherwise),
-    // 1 host, 2 loop graph, 3 persistent kernel; p ranks always host-driven
+    // 1 host, 2 loop graph, 3 persistent kernel, 4 one-cluster search; p ranks always host-driven
     int loop = g->policy.loop;
     if (env_host_loop) loop = 1;
     if (loop == 0) loop = g->arcs_local <= persist_max_arcs() ? 3 : 2;
     if (!mg && g->nparts == 1 && loop != 1) {
-        if (bfs_run_graph(g, root, od, op, parent_out, depth_out, loop == 3)) return;
+        if (bfs_run_graph(g, root, od, op, parent_out, depth_out, loop == 3 ? 1 : loop == 4 ? 2 : 0)) return;
         g->levels.clear();   // deeper than the graph's record capacity: host loop below
         g->run = bfs_run_stats{};
         g->run.root = root;

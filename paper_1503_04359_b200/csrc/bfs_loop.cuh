@@ -408,15 +408,27 @@ struct GridBar {
     }
 };
 
+// Thread-block-cluster barrier (one cluster runs the whole search: the hardware
+// barrier.cluster with release/acquire semantics at cluster scope replaces the
+// atomic-and-spin grid barrier).
+struct ClusterBar {
+    __device__ __forceinline__ void sync() const {
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+    }
+};
+
 __device__ __forceinline__ bool pers_in_front(const uint32_t* front, int32_t u) {
     return (__ldcg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
 
-__global__ void __launch_bounds__(kPersThreads) k_bfs_persistent(
+// Bar = GridBar: one resident wave over every SM; Bar = ClusterBar: ONE thread-block
+// cluster (up to 16 CTAs) whose levels are separated by barrier.cluster.
+template <class Bar, int kThreads>
+__global__ void __launch_bounds__(kThreads) k_bfs_persistent(
     const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
     uint32_t* visited, uint32_t* f0, uint32_t* f1, int64_t words, int2* __restrict__ rec,
     const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, Queue qa, Queue qb,
-    unsigned long long* cnt3, int32_t* big, Ctl* ctl, LevelRec* lrec, GridBar grid) {
+    unsigned long long* cnt3, int32_t* big, Ctl* ctl, LevelRec* lrec, Bar grid) {
     // One grid barrier per level: the counters are triple-buffered (level d accumulates
     // into set d % 3, zeroed by thread 0 two levels ahead), and every thread rolls its own
     // copy of the loop state from them after the barrier (the same arithmetic on the

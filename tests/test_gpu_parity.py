@@ -25,7 +25,9 @@ POLICIES = [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode
             # every level loop (auto picks the persistent kernel for these small graphs)
             dict(mode=0, loop="host"), dict(mode=3, alpha=500, beta=3, loop="host"),
             dict(mode=0, loop="graph"), dict(mode=2, bu_from_level=1, loop="graph"),
-            dict(mode=3, alpha=500, beta=3, loop="graph"), dict(mode=1, loop="graph")]
+            dict(mode=3, alpha=500, beta=3, loop="graph"), dict(mode=1, loop="graph"),
+            dict(mode=0, loop="cluster"), dict(mode=2, bu_from_level=1, loop="cluster"),
+            dict(mode=3, alpha=500, beta=3, loop="cluster")]
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -232,7 +234,7 @@ def test_host_output_buffers():
 
 
 @pytest.mark.parametrize("reindex", [False, True])
-@pytest.mark.parametrize("loop", ["host", "graph", "persistent"])
+@pytest.mark.parametrize("loop", ["host", "graph", "persistent", "cluster"])
 def test_pinned_host_outputs(reindex, loop):
     """pinned host outputs (the e2e leg of bench.py): every entry is overwritten
     (buffers start as garbage), depth == oracle, parents valid, in every level loop
@@ -293,7 +295,7 @@ def test_all_loops_agree_kronecker(reindex):
     g = pkg.Graph.kronecker(14, 16, 11, opts=pkg.default_opts(reindex_by_degree=reindex))
     for r in g.sample_roots(14, 11, 6):
         out = []
-        for loop in ("persistent", "graph", "host"):
+        for loop in ("persistent", "graph", "host", "cluster"):
             g.set_policy(mode=0, alpha=30, beta=24, loop=loop, level_times=True)
             parent, depth = g.run(int(r))
             run, levels = g.stats()
@@ -356,7 +358,7 @@ def _degenerate_cases():
     }
 
 
-@pytest.mark.parametrize("loop", ["persistent", "graph", "host"])
+@pytest.mark.parametrize("loop", ["persistent", "graph", "host", "cluster"])
 @pytest.mark.parametrize("reindex", [False, True])
 def test_degenerate_and_ragged_graphs(loop, reindex):
     """Empty, edgeless, self-loop-only and ragged-size graphs, a long hub row, isolated roots:
