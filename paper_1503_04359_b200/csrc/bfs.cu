@@ -380,13 +380,13 @@ static void build_loop_graph(bfs_graph_s* g) {
     const int64_t nl = g->nl();
     const int64_t words = loop_words(g);
     if (!g->ctl.p) {
-        g->ctl.alloc(sizeof(Ctl) / 8, s);
-        g->lrec.alloc((size_t)kGraphMaxLevels * sizeof(LevelRec) / 8, s);
+        // loop state and step records in one buffer: one read-back per search
+        g->ctl.alloc((sizeof(Ctl) + (size_t)kGraphMaxLevels * sizeof(LevelRec)) / 8, s);
         BFS_CUDA(cudaMallocHost(&g->h_ctl, sizeof(Ctl) + kLrecHead * sizeof(LevelRec)));
         BFS_CUDA(cudaMallocHost(&g->h_lrec, (size_t)kGraphMaxLevels * sizeof(LevelRec)));
     }
     Ctl* ctl = reinterpret_cast<Ctl*>(g->ctl.p);
-    LevelRec* lrec = reinterpret_cast<LevelRec*>(g->lrec.p);
+    LevelRec* lrec = reinterpret_cast<LevelRec*>(g->ctl.p + sizeof(Ctl) / 8);
     unsigned long long* cnt = (unsigned long long*)g->cnt.p;
     unsigned long long* tstate = (unsigned long long*)g->tstate.p;
     const Queue qa{g->q0.p, g->qd0.p}, qb{g->q1.p, g->qd1.p};
@@ -476,6 +476,13 @@ static int64_t persist_max_arcs() {
     return e ? atoll(e) : (int64_t)1 << 22;
 }
 
+// graphs up to this many arcs use the one-cluster search in auto mode (BFS_CLUSTER_MAX_ARCS):
+// K16 (1.5 M arcs) 80 vs 95 us per search; at s20 (31 M arcs) the full-device wave wins
+static int64_t cluster_max_arcs() {
+    const char* e = getenv("BFS_CLUSTER_MAX_ARCS");
+    return e ? atoll(e) : (int64_t)1 << 21;
+}
+
 static int pers_blocks_per_sm() {
     const char* e = getenv("BFS_PERSIST_BLOCKS");   // tuning only
     return e ? std::max(1, atoi(e)) : 1;
@@ -522,6 +529,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             g->loop_key = {bu_long_setting(), bu_dense_setting()};
         }
         if (!g->big.p) g->big.alloc((size_t)(g->arcs_local / kPersBig + 4), s);   // + 2 barrier words
+        if (!g->pcnt.p) g->pcnt.alloc(48, s);
     }
     // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
     const std::vector<int> key{bu_long_setting(), bu_dense_setting()};
@@ -542,27 +550,28 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     const int64_t pw = reset_words(g);
     const bool lt = g->policy.level_times != 0;
     BFS_CUDA(cudaEventRecord(g->ev[0], s));
-    k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr,
-                                                 g->rec.p, qa, g->head.p, (unsigned long long*)g->cnt.p, ctl, g->policy,
-                                                 g->n, g->arcs_global, kGraphMaxLevels, td_claim_min(),
-                                                 (persistent || !g->tile_T) ? (int64_t)-1 : tile_min_setting(),
-                                                 td_small_setting());
-    BFS_CHECK_LAUNCH();
+    const InitArgs ia{g->visited.p, g->skip.p, pw, root, g->reindexed ? g->label.p : nullptr, g->rec.p, qa, g->head.p,
+                      (unsigned long long*)g->cnt.p, ctl, g->policy, g->n, g->arcs_global, kGraphMaxLevels,
+                      td_claim_min(), (persistent || !g->tile_T) ? (int64_t)-1 : tile_min_setting(), td_small_setting(),
+                      persistent ? (unsigned long long*)g->pcnt.p : nullptr,
+                      persistent ? reinterpret_cast<unsigned*>(g->big.p + g->big.count - 2) : nullptr};
+    // the one-cluster search runs the init itself (its barrier needs no memory words)
+    const bool fused_init = mode == 2;
+    if (!fused_init) {
+        k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(ia);
+        BFS_CHECK_LAUNCH();
+    }
     BFS_CUDA(cudaEventRecord(g->ev[2], s));
     if (persistent) {
         const int64_t words = loop_words(g);
         const Queue qb{g->q1.p, g->qd1.p};
-        LevelRec* lrec = reinterpret_cast<LevelRec*>(g->lrec.p);
+        LevelRec* lrec = reinterpret_cast<LevelRec*>(g->ctl.p + sizeof(Ctl) / 8);
         const int32_t* pmap = g->reindexed ? g->ilabel.p : nullptr;
         const int32_t* hpar = g->reindexed ? g->hpar.p : nullptr;
-        unsigned long long* cntp = (unsigned long long*)g->cnt.p;
         // barrier words live in the tail of the big-row list buffer; the three counter sets
         // start at zero except what k_init_dev put in set 0
+        // (zeroed by k_init_dev, which also put the root's counters in set 0)
         unsigned* bar = reinterpret_cast<unsigned*>(g->big.p + g->big.count - 2);
-        BFS_CUDA(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), s));
-        if (!g->pcnt.p) g->pcnt.alloc(48, s);
-        BFS_CUDA(cudaMemsetAsync(g->pcnt.p, 0, 48 * sizeof(int64_t), s));
-        BFS_CUDA(cudaMemcpyAsync(g->pcnt.p, cntp, 16 * sizeof(int64_t), cudaMemcpyDeviceToDevice, s));
         // the grid barrier needs every CTA resident at once: a cooperative launch
         // guarantees it or fails (instead of hanging when other work holds SMs)
         cudaLaunchConfig_t cfg{};
@@ -574,6 +583,8 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         attr[0].val.cooperative = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+        const PersOut po{(od || op) ? (g->reindexed ? 2 : 1) : 0, g->skip.p, g->label.p, g->reindexed ? g->n : nl,
+                         g->n_active, od, op};
         cudaError_t e;
         if (mode == 2) {
             // one cluster: hardware barrier.cluster between phases, guaranteed co-scheduled
@@ -592,12 +603,12 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             e = cudaLaunchKernelEx(&cfg, k_bfs_persistent<ClusterBar, kClusterThreads>, (const int64_t*)g->off.p,
                                    (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p, g->front.p,
                                    g->next.p, words, g->rec.p, pmap, hpar, qa, qb, (unsigned long long*)g->pcnt.p,
-                                   g->big.p, ctl, lrec, ClusterBar{});
+                                   g->big.p, ctl, lrec, ClusterBar{}, po, ia, 1);
         } else {
             e = cudaLaunchKernelEx(&cfg, k_bfs_persistent<GridBar, kPersThreads>, (const int64_t*)g->off.p,
                                    (const int2*)g->head.p, (const int32_t*)g->adj.p, g->visited.p, g->front.p,
                                    g->next.p, words, g->rec.p, pmap, hpar, qa, qb, (unsigned long long*)g->pcnt.p,
-                                   g->big.p, ctl, lrec, GridBar{bar, bar + 1});
+                                   g->big.p, ctl, lrec, GridBar{bar, bar + 1}, po, ia, 0);
         }
         if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorLaunchOutOfResources ||
             e == cudaErrorInvalidClusterSize) {
@@ -605,6 +616,10 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             // same steps from the state k_init_dev wrote
             cudaGetLastError();
             persistent = false;
+            if (fused_init) {
+                k_init_dev<<<grid_for(pw, 256), 256, 0, s>>>(ia);
+                BFS_CHECK_LAUNCH();
+            }
             ensure_loop_graph();
             BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
             ++g->coop_fallbacks;
@@ -615,8 +630,8 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         BFS_CUDA(cudaGraphLaunch(g->loop_exec, s));
     }
     BFS_CUDA(cudaEventRecord(g->ev[3], s));
-    int64_t launches = 1;
-    if (od || op) {
+    int64_t launches = (fused_init && persistent) ? 0 : 1;   // k_init_dev
+    if ((od || op) && !persistent) {   // (the persistent search ran the output pass itself)
         if (g->reindexed) {
             k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
                                                                                    g->rec.p);
@@ -634,17 +649,17 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     if (parent_out && op != parent_out)
         BFS_CUDA(cudaMemcpyAsync(parent_out, op, (size_t)nl * 4, cudaMemcpyDeviceToHost, s));
     // the one read-back of the search: loop state plus the first kLrecHead step records
-    BFS_CUDA(cudaMemcpyAsync(g->h_ctl, g->ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, s));
-    BFS_CUDA(cudaMemcpyAsync(g->h_lrec, g->lrec.p, kLrecHead * sizeof(LevelRec), cudaMemcpyDeviceToHost, s));
+    BFS_CUDA(cudaMemcpyAsync(g->h_ctl, g->ctl.p, sizeof(Ctl) + kLrecHead * sizeof(LevelRec), cudaMemcpyDeviceToHost, s));
     BFS_CUDA(cudaStreamSynchronize(s));
     const Ctl c = *reinterpret_cast<const Ctl*>(g->h_ctl);
     if (c.overflow) return false;
-    if (c.d > kLrecHead) {
-        BFS_CUDA(cudaMemcpyAsync(g->h_lrec + kLrecHead * sizeof(LevelRec) / 8, g->lrec.p + kLrecHead * sizeof(LevelRec) / 8,
-                                 (size_t)(c.d - kLrecHead) * sizeof(LevelRec), cudaMemcpyDeviceToHost, s));
+    const LevelRec* R = reinterpret_cast<const LevelRec*>(g->h_ctl + sizeof(Ctl) / 8);
+    if (c.d > kLrecHead) {   // a deep search: every record
+        BFS_CUDA(cudaMemcpyAsync(g->h_lrec, g->ctl.p + sizeof(Ctl) / 8, (size_t)c.d * sizeof(LevelRec),
+                                 cudaMemcpyDeviceToHost, s));
         BFS_CUDA(cudaStreamSynchronize(s));
+        R = reinterpret_cast<const LevelRec*>(g->h_lrec);
     }
-    const LevelRec* R = reinterpret_cast<const LevelRec*>(g->h_lrec);
     // kernels the loop graph launched for step d (between k_step_begin and k_step_end)
     const int64_t tmin = g->tile_T ? tile_min_setting() : INT64_MAX, tsmall = td_small_setting(), cmin = td_claim_min();
     auto small = [&](int d) { return R[d].m_f <= tsmall && R[d].m_f <= 64 * R[d].n_f; };
@@ -723,11 +738,12 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         const char* e = getenv("BFS_HOST_LOOP");   // A/B experiments only
         return e && e[0] == '1';
     }();
-    // level loop: 0 auto (persistent kernel for small graphs, loop graph otherwise),
+    // level loop: 0 auto (one cluster for small graphs, the persistent kernel up to 2^22 arcs,
+    // the loop graph above),
     // 1 host, 2 loop graph, 3 persistent kernel, 4 one-cluster search; p ranks always host-driven
     int loop = g->policy.loop;
     if (env_host_loop) loop = 1;
-    if (loop == 0) loop = g->arcs_local <= persist_max_arcs() ? 3 : 2;
+    if (loop == 0) loop = g->arcs_local <= cluster_max_arcs() ? 4 : g->arcs_local <= persist_max_arcs() ? 3 : 2;
     if (!mg && g->nparts == 1 && loop != 1) {
         if (bfs_run_graph(g, root, od, op, parent_out, depth_out, loop == 3 ? 1 : loop == 4 ? 2 : 0)) return;
         g->levels.clear();   // deeper than the graph's record capacity: host loop below

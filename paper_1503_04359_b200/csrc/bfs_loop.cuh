@@ -14,40 +14,58 @@
 
 // init on the device: the root's internal label, visited <- skip | root, root
 // record, the first queue, the loop state (policy included)
-__global__ void k_init_dev(uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip, int64_t pw,
-                           int64_t root, const int32_t* __restrict__ label, int2* __restrict__ out, Queue q,
-                           const int2* __restrict__ head, unsigned long long* __restrict__ cnt, Ctl* ctl,
-                           bfs_policy pol, int64_t n, int64_t arcs, int max_levels, int64_t claim_min,
-                           int64_t tile_min, int64_t td_small) {
-    const int64_t ri = label ? (int64_t)__ldg(label + root) : root;
-    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < pw; w += (int64_t)gridDim.x * blockDim.x) {
-        uint32_t x = skip[w];
+struct InitArgs {
+    uint32_t* visited;
+    const uint32_t* skip;
+    int64_t pw, root;
+    const int32_t* label;
+    int2* out;
+    Queue q;
+    const int2* head;
+    unsigned long long* cnt;
+    Ctl* ctl;
+    bfs_policy pol;
+    int64_t n, arcs;
+    int max_levels;
+    int64_t claim_min, tile_min, td_small;
+    unsigned long long* pcnt;   // persistent / cluster search: its three counter sets (zeroed)
+    unsigned* bar;              // grid-barrier words (zeroed)
+};
+
+__device__ __forceinline__ void init_body(const InitArgs& a) {
+    const int64_t ri = a.label ? (int64_t)__ldg(a.label + a.root) : a.root;
+    for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < a.pw; w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t x = a.skip[w];
         if (w == (ri >> 5)) x |= 1u << (ri & 31);
-        visited[w] = x;
+        a.visited[w] = x;
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        for (int i = 0; i < 16; ++i) cnt[i] = 0;
-        out[ri] = make_int2(0, (int32_t)root);
-        const int32_t dg = head[ri].y;
-        queue_put(q, 0, (int32_t)ri, dg);
+        for (int i = 0; i < 16; ++i) a.cnt[i] = 0;
+        a.out[ri] = make_int2(0, (int32_t)a.root);
+        const int32_t dg = a.head[ri].y;
+        queue_put(a.q, 0, (int32_t)ri, dg);
         Ctl c{};
         c.n_f = 1;
         c.m_f = c.m_fc = dg;
         c.root_i = ri;
-        c.alpha = pol.alpha;
-        c.beta = pol.beta;
-        c.n = n;
-        c.arcs = arcs;
+        c.alpha = a.pol.alpha;
+        c.beta = a.pol.beta;
+        c.n = a.n;
+        c.arcs = a.arcs;
         c.have_queue = 1;
-        c.mode = pol.mode;
-        c.bu_from = pol.bu_from_level;
-        c.max_levels = max_levels;
-        c.claim_min = claim_min;
-        c.tile_min = tile_min;
-        c.td_small = td_small;
-        *ctl = c;
+        c.mode = a.pol.mode;
+        c.bu_from = a.pol.bu_from_level;
+        c.max_levels = a.max_levels;
+        c.claim_min = a.claim_min;
+        c.tile_min = a.tile_min;
+        c.td_small = a.td_small;
+        *a.ctl = c;
+        if (a.pcnt)
+            for (int i = 0; i < 48; ++i) a.pcnt[i] = 0;
+        if (a.bar) a.bar[0] = a.bar[1] = 0u;
     }
 }
+__global__ void k_init_dev(InitArgs a) { init_body(a); }
 
 // the step's bookkeeping and direction (the host loop's rule, verbatim); returns m_u(d)
 __device__ __forceinline__ long long step_decide(Ctl& c) {
@@ -381,7 +399,8 @@ __global__ void k_q2b_dev(const Ctl* ctl, Queue qa, Queue qb, uint32_t* __restri
 // Data other blocks wrote during the search is read with ld.global.cg (L1 is not
 // coherent across the grid barrier); the CSR is read-only.
 constexpr int kPersThreads = 256;
-constexpr int kPersBig = 2048;   // rows at least this long are split over the grid
+constexpr int kPersBig = 128;    // rows at least this long are split over the grid (a hub row of a
+                                 // few thousand arcs was 60+ dependent warp steps: ~90 us at K16)
 
 // Grid-wide barrier for a grid no larger than one resident wave (the launch sizes it
 // from the occupancy): arrive on a counter; the last block resets it and bumps the
@@ -421,6 +440,17 @@ __device__ __forceinline__ bool pers_in_front(const uint32_t* front, int32_t u) 
     return (__ldcg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
 
+// the output pass the persistent search runs after its last level (mode 0: none,
+// 1: labels unchanged (emit_body), 2: degree-reindexed (mark_unreached + emit_perm))
+struct PersOut {
+    int mode;
+    const uint32_t* skip;
+    const int32_t* label;
+    int64_t n, n_active;
+    int32_t* depth;
+    int32_t* parent;
+};
+
 // Bar = GridBar: one resident wave over every SM; Bar = ClusterBar: ONE thread-block
 // cluster (up to 16 CTAs) whose levels are separated by barrier.cluster.
 template <class Bar, int kThreads>
@@ -428,7 +458,8 @@ __global__ void __launch_bounds__(kThreads) k_bfs_persistent(
     const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
     uint32_t* visited, uint32_t* f0, uint32_t* f1, int64_t words, int2* __restrict__ rec,
     const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, Queue qa, Queue qb,
-    unsigned long long* cnt3, int32_t* big, Ctl* ctl, LevelRec* lrec, Bar grid) {
+    unsigned long long* cnt3, int32_t* big, Ctl* ctl, LevelRec* lrec, Bar grid, PersOut po, InitArgs ia,
+    int do_init) {
     // One grid barrier per level: the counters are triple-buffered (level d accumulates
     // into set d % 3, zeroed by thread 0 two levels ahead), and every thread rolls its own
     // copy of the loop state from them after the barrier (the same arithmetic on the
@@ -438,6 +469,10 @@ __global__ void __launch_bounds__(kThreads) k_bfs_persistent(
     const int64_t gtid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
     const int64_t gwarp = gtid >> 5, nwarps = nthr >> 5;
+    if (do_init) {   // the search's init in the same kernel (cluster search: one launch per search)
+        init_body(ia);
+        grid.sync();
+    }
     Ctl c;
     {
         const long long* cw = reinterpret_cast<const long long*>(ctl);
@@ -495,9 +530,41 @@ __global__ void __launch_bounds__(kThreads) k_bfs_persistent(
             }
             grid.sync();
             nbig = (int)__ldcg(cnt + C_SCAN);
-            for (int k = 0; k < nbig; ++k) {   // big rows: the whole grid, arc per thread
+            // big rows: up to 4 arcs per thread of a CTA -> one CTA each (round robin);
+            // longer ones -> the whole grid, arc per thread
+            for (int k = blockIdx.x; k < nbig; k += gridDim.x) {
                 const int32_t u = __ldcg(big + k);
                 const int64_t b = __ldg(off + u), e = __ldg(off + u + 1);
+                if (e - b > 4 * (int64_t)blockDim.x) continue;
+                const int32_t pu = pmap ? __ldg(pmap + u) : u;
+                for (int64_t j0 = b + threadIdx.x - lane; j0 < e; j0 += blockDim.x) {
+                    const int64_t j = j0 + lane;
+                    bool win = false;
+                    int32_t v = 0;
+                    if (j < e) {
+                        v = __ldg(adj + j);
+                        const uint32_t bit = 1u << (v & 31);
+                        uint32_t* wp = visited + (v >> 5);
+                        if (!(__ldcg(wp) & bit)) win = !(atomicOr(wp, bit) & bit);
+                    }
+                    const unsigned m = __ballot_sync(kFull, win);
+                    if (m) {
+                        unsigned long long base = 0;
+                        if (lane == 0) base = atomicAdd(cnt + C_NEXT, (unsigned long long)__popc(m));
+                        base = __shfl_sync(kFull, base, 0);
+                        if (win) {
+                            const int32_t vd = __ldg(head + v).y;
+                            queue_put(qn, base + __popc(m & lanemask_lt()), v, vd);
+                            rec[v] = make_int2(lvl, pu);
+                            my_mf += (unsigned long long)vd;
+                        }
+                    }
+                }
+            }
+            for (int k = 0; k < nbig; ++k) {
+                const int32_t u = __ldcg(big + k);
+                const int64_t b = __ldg(off + u), e = __ldg(off + u + 1);
+                if (e - b <= 4 * (int64_t)blockDim.x) continue;
                 const int32_t pu = pmap ? __ldg(pmap + u) : u;
                 for (int64_t j0 = b + gtid - lane; j0 < e; j0 += nthr) {
                     const int64_t j = j0 + lane;
@@ -600,6 +667,16 @@ __global__ void __launch_bounds__(kThreads) k_bfs_persistent(
             if (!cont) *ctl = c;
         }
         if (!cont) break;
+    }
+    // the output pass in the same kernel (saves two launches per search on small graphs)
+    if (po.mode) {
+        if (po.mode == 2) {   // degree-reindexed: reset unreached records, then the permuted pass
+            mark_unreached_body(visited, po.skip, po.n_active, rec);
+            grid.sync();
+            emit_perm_body(rec, po.label, po.n, po.n_active, c.root_i, po.depth, po.parent);
+        } else {
+            emit_body(visited, po.skip, rec, po.n, c.root_i, po.depth, po.parent);
+        }
     }
 }
 

@@ -757,10 +757,9 @@ __global__ void k_b2q(const uint32_t* __restrict__ bm, int64_t words, int64_t lo
 // and need neither the visited lookup nor the record gather.  Everything except the
 // visited bitmap is touched once, so it streams with evict-first hints and the
 // bitmap stays in L2 for the random lookups.
-__global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
-                       const int2* __restrict__ rec, int64_t nl, int64_t root_l, int32_t* __restrict__ depth,
-                       int32_t* __restrict__ parent, const Ctl* ctl) {
-    if (ctl) root_l = ctl->root_i;
+__device__ __forceinline__ void emit_body(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                                          const int2* __restrict__ rec, int64_t nl, int64_t root_l,
+                                          int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nl; v += (int64_t)gridDim.x * blockDim.x) {
         const int64_t w = v >> 5;
         const uint32_t r = visited[w] & ~skip[w];
@@ -770,15 +769,19 @@ __global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __r
         if (parent) parent[v] = o.y;
     }
 }
+__global__ void k_emit(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                       const int2* __restrict__ rec, int64_t nl, int64_t root_l, int32_t* __restrict__ depth,
+                       int32_t* __restrict__ parent, const Ctl* ctl) {
+    emit_body(visited, skip, rec, nl, ctl ? ctl->root_i : root_l, depth, parent);
+}
 
 // Degree-reindexed variant: v runs over ORIGINAL labels and gathers the record of
 // iv = label[v].  Internal labels >= n_active are isolated (the reindex puts them
 // last) and need no gather unless one is the root.  Labels and outputs are touched
 // once and stream with evict-first hints.
-__global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
-                            int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
-                            int32_t* __restrict__ parent, const Ctl* ctl) {
-    if (ctl) root_l = ctl->root_i;
+__device__ __forceinline__ void emit_perm_body(const int2* __restrict__ rec, const int32_t* __restrict__ label,
+                                               int64_t n, int64_t n_active, int64_t root_l,
+                                               int32_t* __restrict__ depth, int32_t* __restrict__ parent) {
     // kEmitV original vertices per thread: 16-byte label loads, then one record
     // gather per non-isolated vertex (k_mark_unreached has reset the records of the
     // unreached ones).  Same-degree vertices keep their original order in the
@@ -836,12 +839,19 @@ __global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restr
     }
 }
 
+__global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restrict__ label, int64_t n,
+                            int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
+                            int32_t* __restrict__ parent, const Ctl* ctl) {
+    emit_perm_body(rec, label, n, n_active, ctl ? ctl->root_i : root_l, depth, parent);
+}
+
 // rec <- (-1, -1) for every vertex of [0, nbits) with degree > 0 that this search did
 // not reach (a few per search in a Kronecker graph: one coalesced pass over the
 // bitmaps, scattered writes for the unreached only), so that the reindexed output
 // pass can take every active vertex's record as is
-__global__ void k_mark_unreached(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
-                                 int64_t nbits, int2* __restrict__ rec) {
+__device__ __forceinline__ void mark_unreached_body(const uint32_t* __restrict__ visited,
+                                                    const uint32_t* __restrict__ skip, int64_t nbits,
+                                                    int2* __restrict__ rec) {
     const int64_t words = (nbits + 31) / 32;
     for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < words; w += (int64_t)gridDim.x * blockDim.x) {
         uint32_t x = ~__ldcs(visited + w) & ~__ldcs(skip + w);
@@ -852,6 +862,10 @@ __global__ void k_mark_unreached(const uint32_t* __restrict__ visited, const uin
             rec[w * 32 + k] = make_int2(-1, -1);
         }
     }
+}
+__global__ void k_mark_unreached(const uint32_t* __restrict__ visited, const uint32_t* __restrict__ skip,
+                                 int64_t nbits, int2* __restrict__ rec) {
+    mark_unreached_body(visited, skip, nbits, rec);
 }
 
 // Output pass of a degree-reindexed search on p ranks: the reindex is partition-local

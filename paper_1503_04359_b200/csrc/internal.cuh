@@ -164,7 +164,7 @@ struct bfs_graph_s {
 
     // device-driven level loop (one GPU): state, per-step records, scan tile states,
     // the instantiated loop graph and pinned mirrors for the one read-back per search
-    bfsb::DevBuf<int64_t> ctl, lrec, tstate;
+    bfsb::DevBuf<int64_t> ctl, tstate;   // ctl: loop state followed by the step records
     bfsb::DevBuf<uint32_t> tctr;
     cudaGraph_t loop_graph = nullptr;
     cudaGraphExec_t loop_exec = nullptr;
