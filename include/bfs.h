@@ -91,8 +91,8 @@ typedef struct {
  *           steps ("a fixed number of steps") return to TD for the rest of the search.
  * level_times != 0 records per-step device times into bfs_level_stats.ms / kernel_ms.
  * loop (who drives the levels): 0 = auto: on one GPU a device-driven loop,
- *   the persistent one-kernel search for graphs up to 2^22 arcs, the CUDA loop graph
- *   (conditional WHILE/IF nodes) above; on p ranks the host (the exchange sizes are
+ *   the one-cluster search for graphs up to 2^21 arcs, the persistent one-kernel
+ *   search up to 2^22 arcs, the CUDA loop graph (conditional WHILE/IF nodes) above; on p ranks the host (the exchange sizes are
  *   host decisions).  1 = host-driven loop (one synchronisation per level).  2 = the
  *   loop graph, 3 = the persistent kernel (one GPU; else host), 4 = the persistent
  *   search as ONE thread-block cluster (up to 16 CTAs; levels separated by the
@@ -230,12 +230,13 @@ bfs_status bfs_graph_destroy(bfs_graph_t g);
 /* ---- multi-GPU (SURVEY e; Alg. 2/3) ----
  * 1D vertex partition: rank r owns [r*nb, min(n, (r+1)*nb)) with
  * nb = ceil(ceil(n/p)/32)*32 (bfs_partition_range).  Per level, bottom-up steps
- * allgather the next-frontier bitmap slices (Alg. 3 PullFrontiers); top-down steps
- * send (vertex, parent) claims for remote vertices to their owners with grouped
- * send/recv after an allgather of the p x p claim counts (Alg. 2 PushFrontiers);
+ * allgather the next-frontier bitmap slices (Alg. 3 PullFrontiers); sparse top-down
+ * steps send (vertex, parent) claims for remote vertices to their owners with grouped
+ * send/recv after an allgather of the p x p claim counts, dense ones (global m_f >=
+ * n/64) send per-peer outbox bitmaps and the parents of those claims follow in one
+ * final aggregation after the last level (Alg. 2 PushFrontiers);
  * the four switch counters are allreduced, so every rank takes the same direction.
- * Parents travel with the top-down claims, so no separate aggregation step is
- * needed (contrast P:79).  With reindex_by_degree the
+ * DESIGN.md section 7.  With reindex_by_degree the
  * reindex is partition-local (the block partition of the original labels
  * first, then each rank permutes its own local IDs by degree), so every rank
  * produces the outputs of its own original labels (n must be divisible by 32*p).

@@ -65,6 +65,14 @@ static int64_t reset_words(bfs_graph_s* g) {
     return pw;
 }
 
+// p ranks: top-down steps whose global m_f reaches this push bitmaps instead of (vertex,
+// parent) claim lists: 8 bytes per claim against (p - 1) slices of nb / 8 bytes; m_f
+// bounds the claims, so n / 64 arcs (BFS_TD_BITMAP_MIN overrides: tests, tuning)
+static int64_t td_bitmap_min(const bfs_graph_s* g) {
+    const char* e = getenv("BFS_TD_BITMAP_MIN");
+    return e ? atoll(e) : std::max<int64_t>(1, g->n / 64);
+}
+
 // top-down steps with at least this many arcs run claim-only + k_td_finish
 // (single partition; BFS_TD_CLAIM_MIN overrides: tuning only)
 static int64_t td_claim_min() {
@@ -795,6 +803,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     const int64_t words = loop_words(g);
     const size_t slice_bytes = mg ? (size_t)(g->nb / 8) : 0;
     uint64_t nvl_total = 0;
+    bool used_bitmap = false;   // some top-down step pushed bitmaps: parent logs to send at the end
+    if (g->plog_cnt.p) BFS_CUDA(cudaMemsetAsync(g->plog_cnt.p, 0, (size_t)p * 8, s));
     std::vector<size_t> sendb(p), recvb(p);
     std::vector<const void*> sendp(p);
     std::vector<void*> recvp(p);
@@ -840,14 +850,31 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             bool claim_mode = false;
             front_ok = false;
             Remote rm{};
+            // dense levels push bitmaps (every rank decides on the same global m_f)
+            const bool bitmap_mode = mg && m_f >= td_bitmap_min(g);
             if (mg) {
                 rm.nb = g->nb;
-                rm.cap = std::max<int64_t>(1, std::min<int64_t>(g->nb, E));
-                ensure(g->out_list, (size_t)(p * rm.cap), s);
                 rm.seen = g->seen.p;
-                rm.out = g->out_list.p;
-                rm.out_cnt = (unsigned long long*)g->out_cnt.p;
-                BFS_CUDA(cudaMemsetAsync(g->out_cnt.p, 0, (size_t)p * sizeof(int64_t), s));
+                if (bitmap_mode) {
+                    if (!g->plog.p) {
+                        g->outbox.alloc((size_t)p * (g->nb / 32), s);
+                        g->inbox.alloc((size_t)p * (g->nb / 32), s);
+                        g->plog.alloc((size_t)p * g->nb, s);
+                        g->plog_cnt.alloc((size_t)p, s);
+                        BFS_CUDA(cudaMemsetAsync(g->plog_cnt.p, 0, (size_t)p * 8, s));   // this search's logs
+                    }
+                    BFS_CUDA(cudaMemsetAsync(g->outbox.p, 0, g->outbox.bytes(), s));
+                    rm.outbox = g->outbox.p;
+                    rm.plog = g->plog.p;
+                    rm.plog_cnt = (unsigned long long*)g->plog_cnt.p;
+                    used_bitmap = true;
+                } else {
+                    rm.cap = std::max<int64_t>(1, std::min<int64_t>(g->nb, E));
+                    ensure(g->out_list, (size_t)(p * rm.cap), s);
+                    rm.out = g->out_list.p;
+                    rm.out_cnt = (unsigned long long*)g->out_cnt.p;
+                    BFS_CUDA(cudaMemsetAsync(g->out_cnt.p, 0, (size_t)p * sizeof(int64_t), s));
+                }
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 1], s));
             // tile mode (td_tile.cuh): heavy frontier rows expanded per tile, the rest below
@@ -916,7 +943,23 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 launches += 2;
             }
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));
-            if (mg) {
+            if (bitmap_mode) {
+                // push as bitmaps (Alg. 2 NextFrontier[P] with parents deferred): slice q
+                // of the outbox to peer q, the received slices ORed into this rank's claims
+                const int64_t nbw = g->nb / 32;
+                for (int q = 0; q < p; ++q) {
+                    sendp[q] = g->outbox.p + (size_t)q * nbw;
+                    sendb[q] = q == me ? 0 : (size_t)nbw * 4;
+                    recvp[q] = g->inbox.p + (size_t)q * nbw;
+                    recvb[q] = q == me ? 0 : (size_t)nbw * 4;
+                    nvl += sendb[q];
+                }
+                g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
+                k_td_inbox<<<grid_for(words, 256), 256, 0, s>>>(g->inbox.p, p, me, nbw, words, g->visited.p, g->head.p,
+                                                                rec, qnxt, cnt, d + 1, g->lo);
+                BFS_CHECK_LAUNCH();
+                ++launches;
+            } else if (mg) {
                 // push: counts matrix (allgather), then claims to their owners (alltoallv)
                 BFS_CUDA(cudaMemcpyAsync(g->cnt_mat.p + (size_t)me * p, g->out_cnt.p, (size_t)p * 8,
                                          cudaMemcpyDeviceToDevice, s));
@@ -1055,6 +1098,37 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     }
     const int ntimed = lt ? (int)std::min<size_t>(g->levels.size(), kMaxTimed) : 0;
     if (lt) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * ntimed], s));
+    if (used_bitmap) {
+        // final aggregation: the parent logs of the bitmap-mode levels to their owners
+        BFS_CUDA(cudaEventRecord(g->ev[3], s));
+        BFS_CUDA(cudaMemcpyAsync(g->cnt_mat.p + (size_t)me * p, g->plog_cnt.p, (size_t)p * 8, cudaMemcpyDeviceToDevice,
+                                 s));
+        g->comm->allgather_inplace(g->cnt_mat.p, (size_t)p * 8, s);
+        BFS_CUDA(cudaMemcpyAsync(g->h_cnt_mat, g->cnt_mat.p, (size_t)p * p * 8, cudaMemcpyDeviceToHost, s));
+        BFS_CUDA(cudaStreamSynchronize(s));
+        int64_t R = 0;
+        for (int q = 0; q < p; ++q) R += q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
+        ensure(g->plog_in, (size_t)std::max<int64_t>(R, 1), s);
+        int64_t roff = 0;
+        uint64_t nvl_agg = 0;
+        for (int q = 0; q < p; ++q) {
+            const int64_t out_q = q == me ? 0 : g->h_cnt_mat[(size_t)me * p + q];
+            const int64_t in_q = q == me ? 0 : g->h_cnt_mat[(size_t)q * p + me];
+            sendp[q] = g->plog.p + (size_t)q * g->nb;
+            sendb[q] = (size_t)out_q * sizeof(int4);
+            recvp[q] = g->plog_in.p + roff;
+            recvb[q] = (size_t)in_q * sizeof(int4);
+            roff += in_q;
+            nvl_agg += sendb[q];
+        }
+        g->comm->alltoallv(sendp.data(), sendb.data(), recvp.data(), recvb.data(), s);
+        if (R) {
+            k_plog_resolve<<<grid_for(R, 256), 256, 0, s>>>(g->plog_in.p, R, rec, g->lo);
+            BFS_CHECK_LAUNCH();
+            ++launches;
+        }
+        nvl_total += nvl_agg;
+    }
     if ((od || op) && g->reindexed && mg) {
         // partition-local reindex: every owned output is produced on this rank
         k_emit_local<<<grid_for(nl, 256), 256, 0, s>>>(g->visited.p, g->skip.p, rec, g->label.p, g->lo, nl, root_l, od,
@@ -1111,6 +1185,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
     g->run.ms_compute = lt ? comp : ms - ms_init;
     g->run.ms_push = push;
     g->run.ms_pull = pull;
+    if (used_bitmap) {
+        float ma = 0;
+        BFS_CUDA(cudaEventElapsedTime(&ma, g->ev[3], g->ev[1]));
+        g->run.ms_aggregate = ma;
+    }
     g->last_root_l = root_l;
     g->run.component_edge_tuples = -1;  // computed lazily by bfs_stats
 }

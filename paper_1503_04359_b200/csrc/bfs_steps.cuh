@@ -47,10 +47,16 @@ __global__ void k_td_chunk_starts(const int64_t* prefix, int64_t F, int64_t nchu
 
 struct Remote {          // p > 1 only
     uint32_t* seen;      // global bitmap: remote vertices this rank already claimed in this BFS
-    int2* out;           // claims (v, parent) for peer q at out[q * cap ...]
+    int2* out;           // list mode: claims (v, parent) for peer q at out[q * cap ...]
     unsigned long long* out_cnt;  // [p]
     int64_t cap;
     int64_t nb;          // partition block size
+    // bitmap mode (dense levels): claims are bits of the global outbox
+    // bitmap (peer q's slice goes to q); (v, parent, level) go to the parent log of the
+    // owner, sent once after the last level
+    uint32_t* outbox;    // null: list mode
+    int4* plog;          // owner q's log at plog[q * nb ...]
+    unsigned long long* plog_cnt;   // [p], kept across the levels of a search
 };
 
 // Top-down step (Alg. 1 TD branch).  Each CTA iteration handles one chunk of
@@ -235,9 +241,17 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
                     const unsigned peers = __match_any_sync(kFull, owner);
                     const int leader = __ffs(peers) - 1;
                     unsigned long long pos = 0;
-                    if (rw && lane == leader) pos = atomicAdd(rm.out_cnt + owner, (unsigned long long)__popc(peers));
-                    pos = __shfl_sync(kFull, pos, leader);
-                    if (rw) rm.out[(int64_t)owner * rm.cap + (int64_t)pos + __popc(peers & lanemask_lt())] = make_int2(v[j], par[j]);
+                    unsigned long long* ctr = rm.outbox ? rm.plog_cnt : rm.out_cnt;
+                    if (rw && lane == leader) pos = atomicAdd(ctr + owner, (unsigned long long)__popc(peers));
+                    pos = __shfl_sync(kFull, pos, leader) + __popc(peers & lanemask_lt());
+                    if (rw) {
+                        if (rm.outbox) {
+                            atomicOr(rm.outbox + (v[j] >> 5), 1u << (v[j] & 31));
+                            rm.plog[(int64_t)owner * rm.nb + (int64_t)pos] = make_int4(v[j], par[j], next_level, 0);
+                        } else {
+                            rm.out[(int64_t)owner * rm.cap + (int64_t)pos] = make_int2(v[j], par[j]);
+                        }
+                    }
                 }
             }
         }
@@ -345,6 +359,66 @@ __global__ void k_td_merge(const int2* __restrict__ in, int64_t R, const int2* _
     }
     my_mf = warp_sum_u64(my_mf);
     if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+}
+
+// Owner side of a bitmap-mode top-down push: the p - 1 received outbox slices are ORed,
+// the bits not yet visited are this rank's new vertices (claimed like local targets);
+// their parents are not known yet: (depth, -1) until the parent logs arrive after the
+// last level (k_plog_resolve).  inbox holds p slices of nbw words (own slice unused).
+__global__ void k_td_inbox(const uint32_t* __restrict__ inbox, int p, int me, int64_t nbw, int64_t words,
+                           uint32_t* __restrict__ visited, const int2* __restrict__ head, int2* __restrict__ out,
+                           const Queue qnext, unsigned long long* __restrict__ cnt, int32_t next_level, int64_t lo) {
+    const int lane = threadIdx.x & 31;
+    unsigned long long my_mf = 0;
+    for (int64_t b0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; b0 < words;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t w = b0 + lane;
+        uint32_t nb = 0;
+        if (w < words) {
+            uint32_t x = 0;
+            for (int q = 0; q < p; ++q)
+                if (q != me) x |= __ldg(inbox + q * nbw + w);
+            const uint32_t vis = visited[w];
+            nb = x & ~vis;
+            if (nb) visited[w] = vis | nb;
+        }
+        const int c = __popc(nb);
+        int inc = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int y = __shfl_up_sync(kFull, inc, d);
+            if (lane >= d) inc += y;
+        }
+        const int tot = __shfl_sync(kFull, inc, 31);
+        if (!tot) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(cnt + C_NEXT, (unsigned long long)tot);
+        base = __shfl_sync(kFull, base, 31);
+        unsigned long long pos = base + (unsigned long long)(inc - c);
+        while (nb) {
+            const int k = __ffs(nb) - 1;
+            nb &= nb - 1;
+            const int64_t vl = w * 32 + k;
+            const int32_t dg = __ldg(head + vl).y;
+            out[vl] = make_int2(next_level, -1);
+            queue_put(qnext, pos++, (int32_t)(lo + vl), dg);
+            my_mf += (unsigned long long)dg;
+        }
+    }
+    my_mf = warp_sum_u64(my_mf);
+    if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+}
+
+// After the last level ("final aggregation"): the parent logs of every claimer,
+// grouped by owner; an entry (v, parent, level) is a valid parent of v iff v was
+// discovered at that level (a claimer may also have claimed v after its owner had
+// discovered it), and only vertices still without a parent take one.
+__global__ void k_plog_resolve(const int4* __restrict__ in, int64_t R, int2* __restrict__ out, int64_t lo) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < R; i += (int64_t)gridDim.x * blockDim.x) {
+        const int4 e = in[i];
+        int2* r = out + (e.x - lo);
+        if (r->x == e.z) atomicCAS(reinterpret_cast<int*>(r) + 1, -1, e.y);
+    }
 }
 
 __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int32_t u) {

@@ -159,6 +159,11 @@ struct bfs_graph_s {
     bfsb::DevBuf<int2> out_list, in_list;  // (vertex, parent) claims
     bfsb::DevBuf<int32_t> flist;     // sparse pull: frontier vertices received from peers
     bfsb::DevBuf<int64_t> out_cnt;   // [p]
+    // bitmap-mode top-down push (dense levels): outbox / inbox bitmaps (p slices of nb/32
+    // words) and the per-owner parent logs (p * nb entries) sent after the last level
+    bfsb::DevBuf<uint32_t> outbox, inbox;
+    bfsb::DevBuf<int4> plog, plog_in;
+    bfsb::DevBuf<int64_t> plog_cnt;  // [p]
     bfsb::DevBuf<int64_t> cnt_mat;   // [p*p] claim counts, row = sender
     int64_t* h_cnt_mat = nullptr;    // pinned mirror
 

@@ -123,7 +123,11 @@ def test_kronecker_s14(p, abc):
     for i, r in enumerate(roots[0]):
         runs, levels = _check(gs, ref, r, pols[i % len(pols)], uv)
         if p > 1:
-            assert sum(x["nvlink_bytes"] for x in levels[0]) == runs[0]["nvlink_bytes"]
+            # the run's bytes = the levels' + the final parent-log aggregation (bitmap pushes)
+            lv_bytes = sum(x["nvlink_bytes"] for x in levels[0])
+            assert lv_bytes <= runs[0]["nvlink_bytes"]
+            if runs[0]["ms_aggregate"] == 0:
+                assert lv_bytes == runs[0]["nvlink_bytes"]
             # bottom-up pulls: bitmap slices when dense, vertex lists when sparse
             for lv in levels[0]:
                 if lv["direction"] == 1 and 4 * lv["frontier"] < slice_bytes * (p - 1):
@@ -227,7 +231,9 @@ def test_degree_reindex_multi(p):
         for run in runs:
             assert run["reached"] == int((want >= 0).sum())
             assert run["component_edge_tuples"] == oracle.component_tuples(uv, want)
-            assert run["ms_aggregate"] == 0
+            # outputs are local; only bitmap-pushed levels leave parent logs to aggregate
+            bitmap = any(x["direction"] == 0 and x["m_f"] >= ref.n // 64 for x in levels[0])
+            assert (run["ms_aggregate"] > 0) == bitmap
     _close(comms, gs)
 
 
@@ -238,3 +244,41 @@ def test_degree_reindex_multi_needs_exact_deal():
                                                     opts=pkg.default_opts(reindex_by_degree=True)), 3)
     for c in comms:
         pkg.bfs_comm_destroy(c)
+
+
+@pytest.mark.parametrize("p", [2, 3, 8])
+@pytest.mark.parametrize("bitmap_min", ["1", "20000"])
+def test_bitmap_push(p, bitmap_min, monkeypatch):
+    """Dense top-down levels push per-peer outbox BITMAPS (Alg. 2 NextFrontier[P]) and defer
+    the parents to a final aggregation of (vertex, parent, level) logs: forced on every
+    top-down step (BFS_TD_BITMAP_MIN=1) or on the dense ones only, with and without the degree
+    reindex, the outputs, parents and counters must match the oracle exactly as in list mode."""
+    monkeypatch.setenv("BFS_TD_BITMAP_MIN", bitmap_min)
+    scale, seed = 14, 4
+    uv, ref = oracle.kron_graph(scale, 16, seed)
+    comms, gs = _build(p, lambda c, s: pkg.Graph.kronecker(scale, 16, seed, comm=c, stream=s))
+    roots = pkg.run_ranks(lambda r: gs[r].sample_roots(scale, seed, 5), p)[0]
+    pols = [dict(mode=1), dict(mode=0), dict(mode=2, bu_from_level=2), dict(mode=0, alpha=2, beta=4),
+            dict(mode=3, alpha=500, beta=2)]
+    slice_bytes = pkg.bfs_partition_range(ref.n, p, 0)[1] // 8
+    bitmap_levels = 0
+    for i, r in enumerate(roots):
+        runs, levels = _check(gs, ref, r, pols[i % len(pols)], uv)
+        for lv in levels[0]:
+            if lv["direction"] == 0 and lv["m_f"] >= int(bitmap_min):
+                bitmap_levels += 1
+                assert lv["nvlink_bytes"] == slice_bytes * (p - 1)
+        if any(lv["direction"] == 0 and lv["m_f"] >= int(bitmap_min) for lv in levels[0]):
+            assert runs[0]["ms_aggregate"] > 0
+    assert bitmap_levels > 0
+    _close(comms, gs)
+    if p in (2, 8):   # degree-reindexed ranks (partition-local labels)
+        lab, pos = oracle.degree_reindex_local(ref, p)
+        comms, gs = _build(p, lambda c, s: pkg.Graph.kronecker(scale, 16, seed, comm=c, stream=s,
+                                                              opts=pkg.default_opts(reindex_by_degree=True)))
+        for r in roots[:3]:
+            parent, depth, runs, levels = _run_all(gs, r, dict(mode=1))
+            want, _ = oracle.bfs(ref, int(r))
+            assert np.array_equal(depth, want)
+            assert not oracle.validate(ref, int(r), depth, parent, ref_depth=want)
+        _close(comms, gs)
