@@ -2,12 +2,14 @@
 
 Each rank takes its vertex range from the library's own partition arithmetic
 (bfs_partition_range, host-only) and runs the partitioned protocol the GPU path
-uses -- TD: per-owner claim lists, an allgather of the p x p claim counts, the
-claims exchanged point to point and merged by the owner (Alg. 2); BU: allgather
-of the next-frontier slices (Alg. 3); an allreduce of the switch counters so that
-every rank picks the same direction -- with numpy standing in for the kernels
-and gloo for NCCL.  Depth must equal the oracle's and the per-step counters the
-emulator's, on both ranks.
+uses -- TD: per-owner (vertex, parent) claim lists, an allgather of the p x p claim
+counts, the claims exchanged point to point and merged by the owner (Alg. 2), or on
+dense levels (global m_f >= bitmap_min) per-peer outbox bitmaps ORed by the owner with
+the parents sent as (vertex, parent, level) logs after the last level; BU:
+allgather of the next-frontier slices (Alg. 3); an allreduce of the switch counters
+so that every rank picks the same direction -- with numpy standing in for the
+kernels and gloo for NCCL.  Depth must equal the oracle's, the parents must
+validate, and the per-step counters must equal the emulator's, on both ranks.
 """
 import os
 import socket
@@ -29,17 +31,41 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
+def _exchange(out, p, rank, width):
+    """point-to-point exchange of per-peer int64 arrays (rows of `width` values) after an
+    allgather of the p x p counts; returns the received arrays per sender"""
+    counts = torch.tensor([len(o) for o in out], dtype=torch.int64)
+    mat = [torch.zeros(p, dtype=torch.int64) for _ in range(p)]
+    dist.all_gather(mat, counts)
+    recv = [torch.zeros((int(mat[q][rank]), width), dtype=torch.int64) for q in range(p)]
+    reqs = []
+    for q in range(p):
+        if q == rank:
+            continue
+        if len(out[q]):
+            reqs.append(dist.isend(torch.tensor(out[q], dtype=torch.int64).reshape(-1, width), q))
+        if recv[q].numel():
+            reqs.append(dist.irecv(recv[q], q))
+    for r in reqs:
+        r.wait()
+    return recv
+
+
+def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0, bitmap_min=None):
     n = ref.n
     deg = ref.degree()
     visited = np.zeros(hi - lo, bool)
     visited[deg[lo:hi] == 0] = True            # skip mask
     depth = np.full(hi - lo, -1, np.int64)
+    parent = np.full(hi - lo, -1, np.int64)
     seen = np.zeros(n, bool)                  # remote claims already sent
+    plog = [[] for _ in range(p)]             # bitmap pushes: (v, parent, level) per owner
+    bitmap_levels = 0
     queue = []
     if lo <= root < hi:
         visited[root - lo] = True
         depth[root - lo] = 0
+        parent[root - lo] = root
         queue = [root]
 
     def allreduce(vals):
@@ -75,7 +101,9 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
         nxt = []
         insp = 0
         if direction == 0:
+            bitmap = bitmap_min is not None and m_f >= bitmap_min   # same global m_f on every rank
             out = [[] for _ in range(p)]
+            outbox = np.zeros(p * nb, bool)
             for u in queue:
                 for v in ref.row(u):
                     insp += 1
@@ -83,30 +111,43 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
                         if not visited[v - lo]:
                             visited[v - lo] = True
                             depth[v - lo] = d + 1
+                            parent[v - lo] = u
                             nxt.append(int(v))
                     elif not seen[v]:
                         seen[v] = True
-                        out[v // nb].append(int(v))
-            counts = torch.tensor([len(o) for o in out], dtype=torch.int64)
-            mat = [torch.zeros(p, dtype=torch.int64) for _ in range(p)]
-            dist.all_gather(mat, counts)                       # p x p claim counts
-            recv = [torch.zeros(int(mat[q][rank]), dtype=torch.int64) for q in range(p)]
-            reqs = []
-            for q in range(p):
-                if q == rank:
-                    continue
-                if len(out[q]):
-                    reqs.append(dist.isend(torch.tensor(out[q], dtype=torch.int64), q))
-                if recv[q].numel():
-                    reqs.append(dist.irecv(recv[q], q))
-            for r in reqs:
-                r.wait()
-            for q in range(p):
-                for v in recv[q].tolist():                     # owner merge
-                    if not visited[v - lo]:
-                        visited[v - lo] = True
-                        depth[v - lo] = d + 1
-                        nxt.append(v)
+                        if bitmap:
+                            outbox[v] = True
+                            plog[v // nb].append((int(v), int(u), d + 1))
+                        else:
+                            out[v // nb].append((int(v), int(u)))
+            if bitmap:
+                bitmap_levels += 1
+                # slice q of the outbox to rank q (point to point; gloo has no all_to_all)
+                parts = [torch.zeros(nb, dtype=torch.uint8) for _ in range(p)]
+                reqs = []
+                for q in range(p):
+                    if q != rank:
+                        reqs.append(dist.isend(torch.from_numpy(outbox[q * nb:(q + 1) * nb].astype(np.uint8)), q))
+                        reqs.append(dist.irecv(parts[q], q))
+                for r in reqs:
+                    r.wait()
+                got_bits = np.zeros(nb, bool)
+                for q in range(p):
+                    if q != rank:
+                        got_bits |= parts[q].numpy().astype(bool)
+                for vl in np.nonzero(got_bits[:hi - lo] & ~visited)[0]:   # owner OR; parent pending
+                    visited[vl] = True
+                    depth[vl] = d + 1
+                    nxt.append(int(lo + vl))
+            else:
+                recv = _exchange(out, p, rank, 2)
+                for q in range(p):
+                    for v, u in recv[q].tolist():              # owner merge
+                        if not visited[v - lo]:
+                            visited[v - lo] = True
+                            depth[v - lo] = d + 1
+                            parent[v - lo] = u
+                            nxt.append(v)
         elif 4 * n_f < (nb // 8) * (p - 1):
             # sparse pull: owned frontier vertices as lists, bitmap rebuilt locally
             counts = [torch.zeros(1, dtype=torch.int64) for _ in range(p)]
@@ -142,6 +183,7 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
                     if front[u]:
                         nxt.append(int(lo + vl))
                         depth[vl] = d + 1
+                        parent[vl] = u
                         break
             for v in nxt:
                 visited[v - lo] = True
@@ -150,7 +192,14 @@ def _partitioned_bfs(ref, root, lo, hi, nb, p, rank, alpha=15, beta=18, mode=0):
         prev, n_f, m_f, m_fc = n_f, got[0], got[1], got[3]
         queue = nxt
         d += 1
-    return depth, steps, sparse_pulls[0]
+    # final aggregation: the parent logs of the bitmap pushes to their owners; a log
+    # entry is a parent iff its level is the vertex's depth
+    recv = _exchange(plog, p, rank, 3)
+    for q in range(p):
+        for v, u, lvl in recv[q].tolist():
+            if depth[v - lo] == lvl and parent[v - lo] == -1:
+                parent[v - lo] = u
+    return depth, parent, steps, sparse_pulls[0], bitmap_levels
 
 
 def _worker(rank, world, port, q):
@@ -166,16 +215,21 @@ def _worker(rank, world, port, q):
             lo, hi = pkg.bfs_partition_range(n, world, rank)
             nb = pkg.bfs_partition_range(n, world, 0)[1]
             for root in sorted({0, n - 1, int(np.argmax(g.degree()))}):
-                for mode, alpha, beta in ((0, 15, 18), (1, 15, 18), (3, 500, 2), (3, 40, 3)):
-                    depth, steps, sp = _partitioned_bfs(g, root, lo, hi, nb, world, rank, alpha, beta, mode)
+                for mode, alpha, beta, bmin in ((0, 15, 18, None), (1, 15, 18, None), (3, 500, 2, None),
+                                                (3, 40, 3, None), (1, 15, 18, 1), (0, 15, 18, 40)):
+                    depth, parent, steps, sp, bl = _partitioned_bfs(g, root, lo, hi, nb, world, rank, alpha, beta,
+                                                                    mode, bmin)
                     full = [None] * world
-                    dist.all_gather_object(full, depth.tolist())
+                    dist.all_gather_object(full, (depth.tolist(), parent.tolist()))
                     want, _ = oracle.bfs(g, root)
                     emu = oracle.do_emulate(g, want, alpha, beta, policy=mode, coord_hi=nb)
-                    ok_depth = np.array_equal(np.concatenate(full), want)
+                    d_all = np.concatenate([np.asarray(x[0]) for x in full])
+                    p_all = np.concatenate([np.asarray(x[1]) for x in full]).astype(np.int32)
+                    ok_depth = np.array_equal(d_all, want) and not oracle.validate(g, root, d_all.astype(np.int32),
+                                                                                   p_all, ref_depth=want)
                     emu_steps = list(zip(emu["dir"].tolist(), emu["n_f"].tolist(), emu["discovered"].tolist(),
                                          emu["m_f"].tolist(), emu["m_u"].tolist(), emu["insp"].tolist()))
-                    out.append((ok_depth, steps == emu_steps, sp))
+                    out.append((ok_depth, steps == emu_steps, sp, bl))
         q.put((rank, out))
     finally:
         dist.destroy_process_group()
@@ -195,6 +249,7 @@ def test_two_rank_protocol_gloo():
         pr.join(timeout=60)
     for r in (0, 1):
         assert res[r], "no cases ran"
-        for ok_depth, ok_steps, _ in res[r]:
+        for ok_depth, ok_steps, _, _ in res[r]:
             assert ok_depth and ok_steps
         assert sum(x[2] for x in res[r]) > 0, "the sparse (vertex-list) pull was never exercised"
+        assert sum(x[3] for x in res[r]) > 0, "the bitmap push was never exercised"
