@@ -432,7 +432,7 @@ static void build_loop_graph(bfs_graph_s* g) {
                                     cnt, tstate, g->tctr.p, (const uint32_t*)g->visited.p, hcnt, g->tile_lcnt.p,
                                     (int64_t)g->tile_nwl, h_tile, g->tile_T ? 1 : 0);
     cudaGraphNode_t t2 = add_kernel(T, {t1}, k_scan_dev, g8, dim3(kScanThreads), 0, ctl, qa, qb, (int64_t)0, g->prefix.p,
-                                    tstate, g->tctr.p, g->tile_nh, g->tile_hlist.p, hcnt, 0);
+                                    tstate, g->tctr.p, g->tile_nh, 0);
     cudaGraphNode_t t3 = add_kernel(T, {t2}, k_td_chunk_starts, g8, t256, 0, g->prefix.p, (int64_t)0, (int64_t)0,
                                     g->scratch64.p, ctl);
     cudaGraphNode_t t4 = add_kernel(T, {t3}, k_td_expand<false>, dim3(td_resident_grid<false>()), dim3(kTdThreads), 0,
@@ -442,7 +442,9 @@ static void build_loop_graph(bfs_graph_s* g) {
     if (g->tile_T) {   // heavy frontier rows and the records of a tile-mode step (IF node set by k_td_prep)
         cudaGraphNode_t n_tile;
         cudaGraph_t TT = add_cond(T, {t4}, h_tile, cudaGraphCondTypeIf, &n_tile);
-        cudaGraphNode_t t5 = add_kernel(TT, {}, k_td_tile, dim3(g->tile_units), dim3(kTileThreads), (size_t)g->tile_maxw * 4,
+        cudaGraphNode_t tl = add_kernel(TT, {}, k_tile_list, g8, t256, 0, (const Ctl*)ctl, qa, qb, (int64_t)0,
+                                        g->tile_nh, g->tile_hlist.p, hcnt);
+        cudaGraphNode_t t5 = add_kernel(TT, {tl}, k_td_tile, dim3(g->tile_units), dim3(kTileThreads), (size_t)g->tile_maxw * 4,
                         (const Ctl*)ctl, (const int32_t*)g->tile_start.p, g->tile_T, (const int2*)g->tile_unit.p,
                         (const int32_t*)g->tile_bnd.p, (const int32_t*)g->tile_hlist.p, (const unsigned*)hcnt,
                         (const int64_t*)g->off.p, (const int32_t*)g->adj.p, g->visited.p, pmap, lg, lrec);
@@ -673,7 +675,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     auto small = [&](int d) { return R[d].m_f <= tsmall && R[d].m_f <= 64 * R[d].n_f; };
     auto claimed = [&](int d) { return R[d].dir == 0 && !small(d) && (R[d].m_f >= cmin || R[d].m_f >= tmin); };
     auto step_kernels = [&](int d) -> int64_t {
-        if (R[d].dir == 0) return small(d) ? 1 : 5 + (R[d].m_f >= tmin ? 2 : 0);
+        if (R[d].dir == 0) return small(d) ? 1 : 5 + (R[d].m_f >= tmin ? 3 : 0);
         const bool conv = d == 0 || (R[d - 1].dir == 0 && !claimed(d - 1));   // queue -> bitmap first
         return 1 + (conv ? 2 : 0);
     };
@@ -891,7 +893,7 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                 const TileLog lg = tile_mode ? tile_log(g) : TileLog{};
                 k_scan_dev<<<grid_for((nf_loc + kScanTile - 1) / kScanTile * kScanThreads, kScanThreads), kScanThreads, 0,
                              s>>>(nullptr, qcur, qcur, nf_loc, g->prefix.p, (unsigned long long*)g->tstate.p,
-                                  g->tctr.p, g->tile_nh, g->tile_hlist.p, g->tile_hcnt.p, tile_mode ? 1 : 0);
+                                  g->tctr.p, g->tile_nh, tile_mode ? 1 : 0);
                 BFS_CHECK_LAUNCH();
                 ++launches;
                 int64_t El = E;   // arcs of the edge-balanced expansion (tile mode: light rows)
@@ -917,6 +919,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                         BFS_CHECK_LAUNCH();
                     }
                     if (tile_mode) {
+                        k_tile_list<<<grid_for(nf_loc, 256), 256, 0, s>>>(nullptr, qcur, qcur, nf_loc, g->tile_nh,
+                                                                          g->tile_hlist.p, g->tile_hcnt.p);
+                        BFS_CHECK_LAUNCH();
                         k_td_tile<<<g->tile_units, kTileThreads, (size_t)g->tile_maxw * 4, s>>>(
                             nullptr, g->tile_start.p, g->tile_T, g->tile_unit.p, g->tile_bnd.p, g->tile_hlist.p,
                             g->tile_hcnt.p, g->off.p, g->adj.p, g->visited.p, pmap, lg, nullptr);
@@ -925,10 +930,9 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
                             nullptr, (int32_t)(d + 1), g->tile_wl.p, g->tile_fu.p, g->tile_unit.p, lg, g->visited.p,
                             next, nullptr, rec, nullptr);
                         BFS_CHECK_LAUNCH();
-                        launches += 2;
+                        launches += 3;
                     }
-                    k_td_finish<<<grid_for(words * 32, 256), 256, 0, s>>>(g->visited.p, next, words, g->head.p, qnxt,
-                                                                         cnt);
+                    k_td_finish<<<grid_for(words * 32, 256), 256, 0, s>>>(g->visited.p, next, words, g->head.p, cnt);
                     BFS_CHECK_LAUNCH();
                     launches += 2;
                 } else if (mg)
@@ -990,8 +994,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             }
             std::swap(qcur, qnxt);
             if (claim_mode) {
-                std::swap(front, next);   // the next frontier as a bitmap too: BU needs no q2b
-                front_ok = true;
+                std::swap(front, next);   // the next frontier as a bitmap only: BU needs no q2b,
+                have_queue = false;       // a top-down step builds its queue with b2q
             }
             insp = E;
             scanned = nf_loc;

@@ -106,9 +106,9 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
         c.qsel ^= 1;
         c.have_queue = 1;
         c.front_ok = 0;
-        if (c.claim) {            // the next frontier is also a bitmap (k_td_finish)
+        if (c.claim) {            // the next frontier is a bitmap only (k_td_finish)
             c.fsel ^= 1;
-            c.front_ok = 1;
+            c.have_queue = 0;
         }
     } else {
         c.fsel ^= 1;
@@ -277,7 +277,7 @@ __global__ void k_td_finish_dev(const Ctl* ctl, const uint32_t* __restrict__ vis
                                 uint32_t* __restrict__ f1, int64_t words, const int2* __restrict__ head, Queue qa,
                                 Queue qb, unsigned long long* __restrict__ cnt) {
     if (!ctl->claim) return;
-    td_finish_body(visited, ctl->fsel ? f0 : f1, words, head, ctl->qsel ? qa : qb, cnt);
+    td_finish_body(visited, ctl->fsel ? f0 : f1, words, head, cnt);
 }
 
 // Single-pass exclusive scan of the current queue's degrees (decoupled look-back:
@@ -287,11 +287,10 @@ constexpr int kScanThreads = 256, kScanItems = 8, kScanTile = kScanThreads * kSc
 constexpr unsigned long long kFlagA = 1ull << 62, kFlagP = 2ull << 62, kValMask = (1ull << 62) - 1;
 
 // Tile mode (td_tile.cuh): queue entries with label < nh (heavy rows) count 0 arcs
-// here -- the tiled kernel expands them -- and are listed in hlist (count *hcount).
+// here -- the tiled kernel expands them (k_tile_list lists them).
 __global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue qa, Queue qb, int64_t n_host,
                                                            int64_t* __restrict__ out, unsigned long long* tstate,
-                                                           unsigned int* tctr, int64_t nh, int32_t* __restrict__ hlist,
-                                                           unsigned* __restrict__ hcount, int tile_host) {
+                                                           unsigned int* tctr, int64_t nh, int tile_host) {
     __shared__ long long s_tile, s_excl;
     __shared__ long long s_warp[kScanThreads / 32];
     // loop graph: size and queue from the loop state; host loop: qa holds the queue
@@ -314,19 +313,9 @@ __global__ void __launch_bounds__(kScanThreads) k_scan_dev(const Ctl* ctl, Queue
         long long v[kScanItems], sum = 0;
 #pragma unroll
         for (int k = 0; k < kScanItems; ++k) {
-            v[k] = base + k < n ? (long long)deg[base + k] : 0;
-            if (tile) {
-                const int32_t u = base + k < n ? qv[base + k] : INT32_MAX;
-                const bool heavy = u < nh;
-                const unsigned m = __ballot_sync(kFull, heavy);
-                if (m) {
-                    unsigned pos = 0;
-                    if (lane == __ffs(m) - 1) pos = atomicAdd(hcount, (unsigned)__popc(m));
-                    pos = __shfl_sync(kFull, pos, __ffs(m) - 1);
-                    if (heavy) hlist[pos + __popc(m & lanemask_lt())] = u;
-                }
-                if (heavy) v[k] = 0;
-            }
+            const bool in = base + k < n;
+            const int32_t u = (tile && in) ? qv[base + k] : INT32_MAX;
+            v[k] = (in && u >= nh) ? (long long)deg[base + k] : 0;   // heavy row (u < nh): k_td_tile expands it
             sum += v[k];
         }
         long long inc = sum;

@@ -273,15 +273,15 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
 
 // Second half of a large top-down step run in claim-only mode (single partition): the
 // winners are the bits the claims set (visited now, not in the snapshot taken before the
-// step), read back in vertex order, so their head-record reads (degree: m_f of the next
-// frontier) and queue appends are coalesced instead of scattered.  The snapshot becomes
-// the next frontier bitmap (a bottom-up step that follows needs no queue conversion).
+// step), read back in vertex order: their count (n_f) and their head records' degrees
+// (m_f of the next frontier) are coalesced reads.  The snapshot buffer becomes the next
+// frontier bitmap, the ONLY form of that frontier: the bottom-up step that usually follows
+// needs no conversion, and a top-down one builds its queue from the bitmap (b2q).
 __device__ __forceinline__ void td_finish_body(const uint32_t* __restrict__ visited, uint32_t* __restrict__ snap,
-                                               int64_t words, const int2* __restrict__ head, const Queue qn,
+                                               int64_t words, const int2* __restrict__ head,
                                                unsigned long long* __restrict__ cnt) {
-    // warp per 32-word batch: one queue reservation (atomicAdd) per 1024 vertices
     const int lane = threadIdx.x & 31;
-    unsigned long long my_mf = 0;
+    unsigned long long my_mf = 0, my_n = 0;
     for (int64_t b0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * 32; b0 < words;
          b0 += (((int64_t)gridDim.x * blockDim.x) >> 5) * 32) {
         const int64_t w = b0 + lane;
@@ -290,37 +290,25 @@ __device__ __forceinline__ void td_finish_body(const uint32_t* __restrict__ visi
             nb = __ldcg(visited + w) & ~__ldcg(snap + w);
             snap[w] = nb;
         }
-        const int c = __popc(nb);
-        int inc = c;
-#pragma unroll
-        for (int dd = 1; dd < 32; dd <<= 1) {
-            const int y = __shfl_up_sync(kFull, inc, dd);
-            if (lane >= dd) inc += y;
-        }
-        const int tot = __shfl_sync(kFull, inc, 31);
-        if (!tot) continue;
-        unsigned long long base = 0;
-        if (lane == 0) base = atomicAdd(cnt + C_NEXT, (unsigned long long)tot);
-        base = __shfl_sync(kFull, base, 0);
-        const int excl = inc - c;
-        for (int k = 0; k < 32; ++k) {
+        my_n += (unsigned long long)__popc(nb);
+        unsigned todo = __ballot_sync(kFull, nb != 0u);
+        while (todo) {   // word by word: the 32 lanes read 32 consecutive head records
+            const int k = __ffs(todo) - 1;
+            todo &= todo - 1;
             const uint32_t nk = __shfl_sync(kFull, nb, k);
-            if (!nk) continue;
-            const int ek = __shfl_sync(kFull, excl, k);
-            if ((nk >> lane) & 1u) {
-                const int64_t v = (b0 + k) * 32 + lane;
-                const int32_t dg = __ldg(head + v).y;
-                my_mf += (unsigned long long)dg;
-                queue_put(qn, base + ek + __popc(nk & lanemask_lt()), (int32_t)v, dg);
-            }
+            if ((nk >> lane) & 1u) my_mf += (unsigned long long)__ldg(head + (b0 + k) * 32 + lane).y;
         }
     }
     my_mf = warp_sum_u64(my_mf);
-    if (lane == 0 && my_mf) atomicAdd(cnt + C_MF, my_mf);
+    my_n = warp_sum_u64(my_n);
+    if (lane == 0) {
+        if (my_mf) atomicAdd(cnt + C_MF, my_mf);
+        if (my_n) atomicAdd(cnt + C_NEXT, my_n);
+    }
 }
 __global__ void k_td_finish(const uint32_t* __restrict__ visited, uint32_t* __restrict__ snap, int64_t words,
-                            const int2* __restrict__ head, const Queue qn, unsigned long long* __restrict__ cnt) {
-    td_finish_body(visited, snap, words, head, qn, cnt);
+                            const int2* __restrict__ head, unsigned long long* __restrict__ cnt) {
+    td_finish_body(visited, snap, words, head, cnt);
 }
 
 // Owner side of the top-down push: claims (v, parent) received from peers are

@@ -126,6 +126,32 @@ __device__ __forceinline__ void light_log(const TileLog& lg, bool win, int32_t v
     lg.lpool[((int64_t)w << kWinShift) + pos] = make_int2(v, par);
 }
 
+// The heavy frontier vertices (label < nh) of the current queue into hlist (count
+// *hcount, zeroed by the prologue): warp-aggregated appends.  ctl == nullptr: host loop,
+// qa is the queue and F its length.
+__global__ void k_tile_list(const Ctl* ctl, Queue qa, Queue qb, int64_t F, int64_t nh, int32_t* __restrict__ hlist,
+                            unsigned* __restrict__ hcount) {
+    const int32_t* qv = qa.v;
+    if (ctl) {
+        if (!ctl->tile) return;
+        qv = ctl->qsel ? qb.v : qa.v;
+        F = ctl->n_f;
+    }
+    const int lane = threadIdx.x & 31;
+    for (int64_t b0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) - lane; b0 < F;
+         b0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = b0 + lane;
+        const int32_t u = i < F ? __ldg(qv + i) : INT32_MAX;
+        const bool heavy = u < nh;
+        const unsigned m = __ballot_sync(kFull, heavy);
+        if (!m) continue;
+        unsigned pos = 0;
+        if (lane == __ffs(m) - 1) pos = atomicAdd(hcount, (unsigned)__popc(m));
+        pos = __shfl_sync(kFull, pos, __ffs(m) - 1);
+        if (heavy) hlist[pos + __popc(m & lanemask_lt())] = u;
+    }
+}
+
 // One CTA per work unit (grid = number of units).  A unit is (tile t, part s of S):
 // a tile whose arc mass exceeds the per-unit target (the hub labels) is split over S
 // CTAs, part s taking heavy-list entries s, s + S, ...; each part claims in its own
@@ -305,6 +331,8 @@ k_tile_rec(const Ctl* ctl, int32_t level_in, const int2* __restrict__ wl, const 
     unsigned any = lg.lcnt[blockIdx.x];
     for (int u = u0; u < u0 + parts; ++u) any |= lg.cnt[(int64_t)u * kMaxWin + k];
     if (!any) return;   // no winner in this window
+    for (int i = threadIdx.x; i < (v1 - v0); i += kWinThreads) s_p[i] = -1;
+    __syncthreads();
     for (int u = u0; u <= u0 + parts; ++u) {
         const bool light = u == u0 + parts;
         const unsigned n = light ? lg.lcnt[blockIdx.x] : lg.cnt[(int64_t)u * kMaxWin + k];
@@ -312,7 +340,9 @@ k_tile_rec(const Ctl* ctl, int32_t level_in, const int2* __restrict__ wl, const 
                               : lg.pool + lg.base[u] + ((int64_t)k << kWinShift);
         for (unsigned i = threadIdx.x; i < n; i += kWinThreads) {
             const int2 e = __ldcs(P + i);
-            s_p[e.x - v0] = e.y;
+            // a vertex two parts of a split tile both claimed has two (valid) entries: the
+            // larger parent label wins, deterministically
+            atomicMax(s_p + (e.x - v0), e.y);
         }
     }
     __syncthreads();
