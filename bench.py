@@ -429,8 +429,7 @@ def main():
         with open(tpath) as f:
             tj = json.load(f)
         traffic = tj.get("k_bu_batch" if dom == "bu" else "k_td_expand")
-        traffic_src = ("profiles/ncu_traffic_%s.json: mean DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) "
-                       "per launch of ONE captured root (%s; %s), not the benched roots"
+        traffic_src = ("profiles/ncu_traffic_%s.json (%s): %s; a capture, not this run's roots"
                        % (args.config, tj.get("_source", "?"), tj.get("_note", "")))
     total_ms = sum(times)
     share = kms / total_ms if total_ms else 0.0
