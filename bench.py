@@ -245,7 +245,7 @@ def rank_memory(scale: int, ef: int, p: int, reindex: bool) -> dict:
     if p > 1:
         steady += 8 * n + 8 * nl
     elif reindex:
-        steady += int(4.3e9 * (n / 2 ** 29))   # tile index + record log, measured at K29
+        steady += int(6.4e9 * (n / 2 ** 29))   # tile index 2.3 GB + record logs 2 x 2 GB at K29
     peak = 8 * raw + 12 * nl + (8 * n if reindex else 0)
     return {"steady_gb": round(steady / 1e9, 1), "build_peak_gb": round(max(steady, peak) / 1e9, 1)}
 
