@@ -231,7 +231,9 @@ def rank_memory(scale: int, ef: int, p: int, reindex: bool) -> dict:
     """Device bytes one rank needs: n = 2^scale, nl = n/p owned
     vertices, raw arcs per rank = 2 * ef * n / p (each tuple is two arcs).
     steady: adjacency 4/arc + per owned vertex off 8, head 8, deg_raw 4, queues 16,
-    prefix 8, records 8 (+ hpar 4 when reindexed) + global arrays label/ilabel 8n (when
+    prefix 8, records 8 (+ hpar 4 when reindexed), bottom-up second-probe planes 32 per
+    row with arcs (2 planes x 16 B; nl rows, n_active ~ 0.44 n on one reindexed GPU)
+    + global arrays label/ilabel 8n (when
     reindexed) + bitmaps (visited, skip: nl/8 each; front, next, seen: n/8 each) + the
     top-down claim lists (p ranks: up to 8 bytes per owned-vertex slot of every peer,
     8 nb p = 8n, plus the receive side) + the tile index (one GPU, reindexed: ~2.3 GB at
@@ -242,6 +244,7 @@ def rank_memory(scale: int, ef: int, p: int, reindex: bool) -> dict:
     raw = 2 * ef * n // p
     steady = 4 * raw + nl * (8 + 8 + 4 + 16 + 8 + 8 + (4 if reindex else 0)) + (8 * n if reindex else 0)
     steady += 2 * nl // 8 + 3 * n // 8
+    steady += 32 * (int(0.44 * nl) if (reindex and p == 1) else nl)
     if p > 1:
         steady += 8 * n + 8 * nl
     elif reindex:

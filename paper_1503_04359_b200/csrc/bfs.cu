@@ -49,6 +49,15 @@ int grid_for(int64_t items, int threads, int per_sm = 8) {
     return (int)std::max<int64_t>(1, std::min(b, cap));
 }
 
+// Planes of bottom-up second-probe blocks used (arcs 1+4p..4+4p of every row,
+// build.cu k_nb4): all that were built unless BFS_BU_NB4 asks for fewer (tuning only)
+static int bu_nbp(const bfs_graph_s* g) {
+    const char* e = getenv("BFS_BU_NB4");
+    const int want = e ? std::max(0, atoi(e)) : g->nb4_planes;
+    return g->nb4.p ? std::min(want, g->nb4_planes) : 0;
+}
+static const int4* bu_nb4(const bfs_graph_s* g) { return bu_nbp(g) ? g->nb4.p : nullptr; }
+
 // Bitmap words a search touches.  With the degree reindex every vertex >= n_active is
 // isolated: its visited bit is its skip bit forever (no step writes it), it is never a
 // frontier vertex, so the steps, conversions and the per-search visited reset cover
@@ -464,8 +473,8 @@ static void build_loop_graph(bfs_graph_s* g) {
     cudaGraphNode_t u1 = add_kernel(C, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
     add_kernel(C, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
     add_kernel(U, {}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
-               g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo, (int32_t)0,
-               cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
+               g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, bu_nb4(g), g->nb4_rows,
+               bu_nbp(g), words, g->lo, (int32_t)0, cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
     BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
     g->loop_graph = G;
 }
@@ -536,13 +545,13 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     if (persistent) {
         if (!g->ctl.p) {   // the state buffers (the graph itself is the fallback)
             build_loop_graph(g);
-            g->loop_key = {bu_long_setting(), bu_dense_setting()};
+            g->loop_key = {bu_long_setting(), bu_dense_setting(), bu_nbp(g)};
         }
         if (!g->big.p) g->big.alloc((size_t)(g->arcs_local / kPersBig + 4), s);   // + 2 barrier words
         if (!g->pcnt.p) g->pcnt.alloc(48, s);
     }
     // the graph bakes the tuning knobs into its kernel arguments: rebuild if they changed
-    const std::vector<int> key{bu_long_setting(), bu_dense_setting()};
+    const std::vector<int> key{bu_long_setting(), bu_dense_setting(), bu_nbp(g)};
     auto ensure_loop_graph = [&] {
         if (g->loop_exec && g->loop_key != key) {
             BFS_CUDA(cudaStreamSynchronize(s));
@@ -1069,8 +1078,8 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
             const int bu_grid = grid_for(nbatches * 32, kBuWarps * 32, kBuCtas);
             const int grab = (int)std::max<int64_t>(1, nbatches / ((int64_t)bu_grid * kBuWarps * 8));
             k_bu_batch<<<bu_grid, kBuWarps * 32, 0, s>>>(g->off.p, g->head.p, g->adj.p, g->visited.p, front, next, rec,
-                                                         pmap, g->reindexed ? g->hpar.p : nullptr, words, g->lo,
-                                                         d + 1, cnt, grab, bu_long_setting(), bu_dense_setting(), nullptr,
+                                                         pmap, g->reindexed ? g->hpar.p : nullptr, bu_nb4(g), g->nb4_rows,
+                                                         bu_nbp(g), words, g->lo, d + 1, cnt, grab, bu_long_setting(), bu_dense_setting(), nullptr,
                                                          nullptr);
             BFS_CHECK_LAUNCH();
             if (timed) BFS_CUDA(cudaEventRecord(g->lev_ev[4 * d + 2], s));

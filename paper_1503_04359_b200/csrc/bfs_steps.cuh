@@ -448,14 +448,15 @@ constexpr int kBuCtas = 4;     // resident CTAs per SM (launch bound and grid; 5
 constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (aligned vector loads: 2, 4 or 8) and probes per round
+constexpr int kNbIlp = 2;     // listed rows per lane in flight in the second-probe phase
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
 __global__ void __launch_bounds__(kBuWarps * 32, kBuCtas)
 k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const int32_t* __restrict__ adj,
            uint32_t* __restrict__ visited,
            const uint32_t* __restrict__ front_in, uint32_t* __restrict__ next_in, int2* __restrict__ out,
-           const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, int64_t words, int64_t lo,
-           int32_t next_level,
+           const int32_t* __restrict__ pmap, const int32_t* __restrict__ hpar, const int4* __restrict__ nb4,
+           int64_t nb4_rows, int nbp, int64_t words, int64_t lo, int32_t next_level,
            unsigned long long* __restrict__ cnt, int grab, int blong, int dense_u, const Ctl* ctl,
            LevelRec* lrec) {
     __shared__ uint16_t s_list[kBuWarps][1024];
@@ -604,7 +605,62 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             }
         }
         __syncwarp();
+        int skip0 = 1;   // arcs already probed per listed row
+        for (int pl = 0; nb4 && pl < nbp && M > 0; ++pl) {
+            // 3a''. second probes: arcs 1+4pl .. 4+4pl of every row still listed, from the
+            //      dense 16-byte block of plane pl (nb4[pl * nb4_rows + v]) read along the
+            //      list (consecutive misses share sectors) instead of an offsets load plus
+            //      a row-aligned adjacency sector per row -- at a hub-frontier level most
+            //      rows miss and most are short.  Rows with arcs past the plane and no hit
+            //      stay listed for the next plane or for 3b.
+            const int4* pb = nb4 + (int64_t)pl * nb4_rows;
+            const int first = 1 + 4 * pl;
+            int M2 = 0;
+            for (int t0 = 0; t0 < M; t0 += 32 * kNbIlp) {
+                int32_t sv[kNbIlp], dg[kNbIlp];
+                int4 x[kNbIlp];
+#pragma unroll
+                for (int k = 0; k < kNbIlp; ++k) {
+                    const int idx = t0 + k * 32 + lane;
+                    sv[k] = idx < M ? (int32_t)list[idx] : -1;
+                }
+#pragma unroll
+                for (int k = 0; k < kNbIlp; ++k) {
+                    dg[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]).y : 0;
+                    x[k] = sv[k] >= 0 ? __ldg(pb + vbase + sv[k]) : make_int4(-1, -1, -1, -1);
+                }
+                __syncwarp();  // the block is in registers before survivors overwrite it
+#pragma unroll
+                for (int k = 0; k < kNbIlp; ++k) {
+                    const int nv = min(dg[k] - first, 4);   // arcs of the block inside the row
+                    const bool h0 = nv > 0 && in_front(front, x[k].x);
+                    const bool h1 = nv > 1 && in_front(front, x[k].y);
+                    const bool h2 = nv > 2 && in_front(front, x[k].z);
+                    const bool h3 = nv > 3 && in_front(front, x[k].w);
+                    const int kh = h0 ? 0 : h1 ? 1 : h2 ? 2 : h3 ? 3 : -1;
+                    if (sv[k] >= 0) {
+                        if (kh >= 0) {
+                            const int32_t hu = kh == 0 ? x[k].x : kh == 1 ? x[k].y : kh == 2 ? x[k].z : x[k].w;
+                            my_insp += (unsigned long long)(kh + 1);
+                            __stcs(out + vbase + sv[k], make_int2(next_level, pmap ? pmap[hu] : hu));
+                            atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
+                            my_mf += (unsigned long long)dg[k];
+                        } else {
+                            my_insp += (unsigned long long)nv;
+                        }
+                    }
+                    const bool miss = sv[k] >= 0 && kh < 0 && dg[k] > first + 4;
+                    const unsigned mm = __ballot_sync(kFull, miss);
+                    if (miss) list[M2 + __popc(mm & lanemask_lt())] = (uint16_t)sv[k];
+                    M2 += __popc(mm);
+                }
+            }
+            M = M2;
+            skip0 = first + 4;
+            __syncwarp();
+        }
         // 3b. rows that missed: each lane keeps kBuSlots rows in flight from position 1
+        //     (1 + 4 nbp after 3a'')
         //     on and advances all of them each round (independent adj[j] loads, then
         //     independent frontier probes), refilling a slot as soon as its row
         //     resolves (the paper's "virtual warp" of one lane per vertex).
@@ -622,8 +678,9 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                     sv[s] = list[t];
                     t += 32;
                     sd[s] = __ldcs(head + vbase + sv[s]).y;
-                    sj[s] = __ldcs(off + vbase + sv[s]) + 1;
-                    se[s] = sj[s] - 1 + sd[s];
+                    const int64_t o = __ldcs(off + vbase + sv[s]);
+                    sj[s] = o + skip0;
+                    se[s] = o + sd[s];
                     sa[s] = true;
                 }
             }
@@ -694,8 +751,9 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                         sv[s] = list[t];
                         t += 32;
                         sd[s] = __ldcs(head + vbase + sv[s]).y;
-                        sj[s] = __ldcs(off + vbase + sv[s]) + 1;
-                        se[s] = sj[s] - 1 + sd[s];
+                        const int64_t o = __ldcs(off + vbase + sv[s]);
+                        sj[s] = o + skip0;
+                        se[s] = o + sd[s];
                         sa[s] = true;
                     }
                 }

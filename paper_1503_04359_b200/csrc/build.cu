@@ -169,6 +169,28 @@ __global__ void k_head_parent(const int2* head, const int32_t* ilabel, int64_t n
     }
 }
 
+// nb4[v] = arcs 1..4 of row v (-1 past the degree): the bottom-up step probes them
+// for the rows that miss on the first arc, reading 16 dense bytes per row along its
+// miss list instead of the row's offsets and a row-aligned adjacency sector
+__global__ void k_nb4(const int64_t* off, const int32_t* adj, int64_t rows, int planes, int4* nb4) {
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < rows; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = off[v], d = off[v + 1] - b;
+        for (int p = 0; p < planes; ++p) {
+            const int64_t k = 1 + 4 * p;
+            nb4[p * rows + v] = make_int4(d > k ? adj[b + k] : -1, d > k + 1 ? adj[b + k + 1] : -1,
+                                          d > k + 2 ? adj[b + k + 2] : -1, d > k + 3 ? adj[b + k + 3] : -1);
+        }
+    }
+}
+
+// planes of second-probe blocks built (BFS_NB_PLANES, default 2: arcs 1..8; 16 bytes
+// per plane and row).  K29 same-box A/B, 64 roots: 0 planes 1583 GTEPS, 1: 1693,
+// 2: 1707, 3: 1706 (profiles/r02_nb4_ab.txt)
+static int nb_planes_setting() {
+    const char* e = getenv("BFS_NB_PLANES");
+    return e ? std::max(0, std::min(8, atoi(e))) : 2;
+}
+
 // Degree reindex on p ranks ("after partitioning ... permutation of local IDs";
 // the oracle's orc_degree_reindex_local): the 1D block partition of the ORIGINAL labels
 // comes first, then every block numbers its own vertices by (degree desc, ID asc).  A
@@ -776,6 +798,17 @@ static void finish_graph(bfs_graph_s* g) {
     if (g->reindexed) {
         g->hpar.alloc((size_t)std::max<int64_t>(nl, 1), s);
         k_head_parent<<<grid_for(nl, 256), 256, 0, s>>>(g->head.p, g->ilabel.p, nl, g->hpar.p);
+        BFS_CHECK_LAUNCH();
+    }
+    // one GPU, reindexed: rows >= n_active are empty and never listed
+    const bool mg = g->comm && g->comm->nranks > 1;
+    const int64_t rows = (g->reindexed && !mg) ? g->n_active : nl;
+    g->nb4_planes = nb_planes_setting();
+    g->nb4_rows = rows;
+    g->nb4.reset();
+    if (g->nb4_planes > 0) {
+        g->nb4.alloc((size_t)std::max<int64_t>(rows * g->nb4_planes, 1), s);
+        k_nb4<<<grid_for(rows, 256), 256, 0, s>>>(g->off.p, g->adj.p, rows, g->nb4_planes, g->nb4.p);
         BFS_CHECK_LAUNCH();
     }
     BFS_CUDA(cudaStreamSynchronize(s));

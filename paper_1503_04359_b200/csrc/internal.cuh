@@ -134,6 +134,10 @@ struct bfs_graph_s {
     bfsb::DevBuf<int2> head;        // [nl] (first neighbour or -1, degree): the bottom-up fast path,
                                     // and the degree of a vertex discovered top-down
     bfsb::DevBuf<int32_t> hpar;     // [nl] reindexed only: ORIGINAL label of the first neighbour
+    bfsb::DevBuf<int4> nb4;         // [planes][nb4_rows] plane p: arcs 1+4p..4+4p of each row (-1 past
+                                    // the degree): the bottom-up second probes read along the miss list
+    int64_t nb4_rows = 0;
+    int nb4_planes = 0;
     // reindex (identity when absent)
     bool reindexed = false;
     int64_t n_active = 0;            // reindexed: labels >= n_active are isolated

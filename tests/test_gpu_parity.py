@@ -470,3 +470,27 @@ def test_device_validator_matches_oracle_validator(reindex, rows):
             assert got == want, (kind, got, want)
             assert set(pkg.bfs_validate(g.h, r, p, d)) == want          # host buffers
     g.close()
+
+
+@pytest.mark.parametrize("nb4", ["2", "1", "0"])
+@pytest.mark.parametrize("loop", ["graph", "host"])
+def test_bottomup_second_probe_blocks(nb4, loop, monkeypatch):
+    """Bottom-up rows that miss on the first arc probe arcs 1..4 from the dense nb4 block
+    (phase 3a'' of k_bu_batch, planes of 4 arcs) and continue in the CSR after the last plane; BFS_BU_NB4=0 takes the
+    CSR from arc 1.  Both must give the emulator's counters, inspections and first
+    frontier neighbours (every fixture has rows of degree 2..6 around the block edge)."""
+    monkeypatch.setenv("BFS_BU_NB4", nb4)
+    for name in ("skewed", "random", "grid", "cube", "union", "clique"):
+        n, uv = FIXTURES[name]
+        g = pkg.Graph.from_edges(uv, n)
+        ref = oracle.build_csr(n, uv, dedup=True, drop_self_loops=True, sort_rows=True)
+        for root in sorted({0, n - 1, int(np.argmax(ref.degree()))}):
+            for pol in (dict(mode=1), dict(mode=2, bu_from_level=1), dict(mode=0, alpha=2, beta=4)):
+                _check_run(g, ref, root, dict(loop=loop, **pol), uv)
+        g.close()
+    uv, ref = oracle.kron_graph(14, 16, 5)
+    g = pkg.Graph.kronecker(14, 16, 5, opts=pkg.default_opts(reindex_by_degree=True))
+    for r in g.sample_roots(14, 5, 4):
+        _check_outputs(g, ref, int(r), dict(loop=loop, mode=1))
+        _check_outputs(g, ref, int(r), dict(loop=loop, mode=0, alpha=30, beta=1000))
+    g.close()

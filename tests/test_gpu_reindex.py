@@ -118,3 +118,20 @@ def test_degree_row_order(scale, abc, seed):
     for i, r in enumerate(g.sample_roots(scale, seed, 6)):
         _check(g, ref, ref, ident, r, [dict(mode=0), dict(mode=1), dict(mode=2, bu_from_level=1)][i % 3], uv)
     g.close()
+
+
+@pytest.mark.parametrize("nb4", ["2", "1", "0"])
+@pytest.mark.parametrize("loop", ["graph", "host"])
+def test_reindex_bottomup_second_probes(nb4, loop, monkeypatch):
+    """the nb4 second-probe phase on a relabeled graph (parents through ilabel):
+    counters, inspections and bottom-up parents equal the emulator's on the relabeled CSR"""
+    monkeypatch.setenv("BFS_BU_NB4", nb4)
+    scale, seed = 13, 4
+    g = pkg.Graph.kronecker(scale, 16, seed, oracle.KRON_ABC, opts=pkg.default_opts(**REIDX))
+    uv, ref = oracle.kron_graph(scale, 16, seed, oracle.KRON_ABC)
+    new, pos = oracle.degree_reindex(ref, 1)
+    rel = oracle.relabel_csr(ref, new, pos)
+    for i, r in enumerate(g.sample_roots(scale, seed, 4)):
+        pol = [dict(mode=0, alpha=30, beta=1000), dict(mode=1), dict(mode=2, bu_from_level=1)][i % 3]
+        _check(g, ref, rel, new, r, dict(loop=loop, **pol), uv)
+    g.close()

@@ -38,11 +38,18 @@ for rep in range(2):
     for val in a.values.split(","):
         os.environ[a.var] = val
         rates = []
+        parts = [0.0, 0.0, 0.0]   # init, level loop, output pass (device ms, summed)
         for r in roots:
             pkg.bfs_run(g.h, int(r), parent, depth)
             run, _ = g.stats(tuples=int(r) not in edges)
             if int(r) not in edges:
                 edges[int(r)] = run["component_edge_tuples"]
             rates.append(edges[int(r)] / (run["ms_total"] * 1e-3) / 1e9)
+            parts[0] += run["ms_init"]
+            parts[1] += run["ms_compute"]
+            parts[2] += run["ms_total"] - run["ms_init"] - run["ms_compute"]
         if rep == 1:
-            print(json.dumps({a.var: val, "gteps": round(bench.hmean(rates), 2)}), flush=True)
+            k = len(roots)
+            print(json.dumps({a.var: val, "gteps": round(bench.hmean(rates), 2),
+                              "ms_init": round(parts[0] / k, 4), "ms_loop": round(parts[1] / k, 4),
+                              "ms_output": round(parts[2] / k, 4)}), flush=True)
