@@ -651,6 +651,9 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
     BFS_CUDA(cudaEventRecord(g->ev[3], s));
     int64_t launches = (fused_init && persistent) ? 0 : 1;   // k_init_dev
     if ((od || op) && !persistent) {   // (the persistent search ran the output pass itself)
+        const int64_t dw = words_of(g->reindexed ? g->n_active : nl);
+        k_l2_demote<<<grid_for((dw + 31) / 32, 256), 256, 0, s>>>(g->front.p, g->next.p, dw);
+        ++launches;
         if (g->reindexed) {
             k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
                                                                                    g->rec.p);
@@ -1149,6 +1152,11 @@ void bfs_run_impl(bfs_graph_s* g, int64_t root, int32_t* parent_out, int32_t* de
         BFS_CHECK_LAUNCH();
         ++launches;
     } else if (od || op) {
+        if (!mg) {
+            const int64_t dw = words_of(g->reindexed ? g->n_active : nl);
+            k_l2_demote<<<grid_for((dw + 31) / 32, 256), 256, 0, s>>>(g->front.p, g->next.p, dw);
+            ++launches;
+        }
         if (g->reindexed) {
             k_mark_unreached<<<grid_for(words_of(g->n_active), 256), 256, 0, s>>>(g->visited.p, g->skip.p, g->n_active,
                                                                                    rec);

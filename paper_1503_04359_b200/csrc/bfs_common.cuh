@@ -69,6 +69,25 @@ struct LevelRec {
     int dir, pad;
 };
 
+// L2 eviction-priority hints: ld.global.nc with an L2::cache_hint policy from
+// createpolicy (the policy lives in a uniform register; the .L2::evict_* qualifiers
+// alone are only accepted on 256-bit loads).  The bottom-up step keeps the frontier
+// bitmap resident (evict_last) against the once-read streams.
+__device__ __forceinline__ uint64_t l2_evict_last() {
+    uint64_t k;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(k));
+    return k;
+}
+// back to normal priority after the search (the output pass then has all of L2)
+__device__ __forceinline__ void l2_demote_line(const void* p) {
+    asm volatile("applypriority.global.L2::evict_normal [%0], 128;" ::"l"(p) : "memory");
+}
+__device__ __forceinline__ uint32_t ldh(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 __device__ __forceinline__ unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

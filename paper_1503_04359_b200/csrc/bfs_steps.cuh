@@ -412,6 +412,9 @@ __global__ void k_plog_resolve(const int4* __restrict__ in, int64_t R, int2* __r
 __device__ __forceinline__ bool in_front(const uint32_t* __restrict__ front, int32_t u) {
     return (__ldg(front + (u >> 5)) >> (u & 31)) & 1u;
 }
+__device__ __forceinline__ bool in_front_p(const uint32_t* __restrict__ front, uint64_t pol, int32_t u) {
+    return (ldh(front + (u >> 5), pol) >> (u & 31)) & 1u;
+}
 
 constexpr int kBuLongDefault = 64;   // B200 sweep: 8 -> 64 is +1%; the warp path stays for hub rows
 // lane-serial probes before a row is handed to the whole warp (BFS_BU_LONG: tuning only)
@@ -480,6 +483,10 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
     uint16_t* list = s_list[wid];
     uint32_t* nbw = s_nb[wid];
     const int64_t wbase = lo >> 5;
+    // frontier probes with an L2 evict_last policy, so the bitmap outlives the once-read
+    // head records, planes and rows streaming through L2 (K29 same-box A/B: loop 3.40 ->
+    // 3.29 ms per search; profiles/r02_l2hint_ab.txt)
+    const uint64_t pk = l2_evict_last();
     const int64_t nbatches = (words + 31) / 32;
     unsigned long long my_nf = 0, my_mf = 0, my_insp = 0, my_scan = 0;
     // batches are claimed `grab` at a time from the global counter (one atomic per
@@ -529,7 +536,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                 for (int j = 0; j < kBuIlp; ++j) po[j] = (hpar && sv[j] >= 0) ? __ldg(hpar + vbase + sv[j]) : hd[j].x;
                 bool hit[kBuIlp];
 #pragma unroll
-                for (int j = 0; j < kBuIlp; ++j) hit[j] = hd[j].y > 0 && in_front(front, hd[j].x);
+                for (int j = 0; j < kBuIlp; ++j) hit[j] = hd[j].y > 0 && in_front_p(front, pk, hd[j].x);
 #pragma unroll
                 for (int j = 0; j < kBuIlp; ++j) {
                     if (hd[j].y > 0) my_insp += 1;
@@ -587,7 +594,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                 for (int k = 0; k < kBuIlp; ++k) po[k] = (hpar && sv[k] >= 0) ? __ldg(hpar + vbase + sv[k]) : hd[k].x;
                 bool hit[kBuIlp];
 #pragma unroll
-                for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front(front, hd[k].x);
+                for (int k = 0; k < kBuIlp; ++k) hit[k] = hd[k].y > 0 && in_front_p(front, pk, hd[k].x);
                 __syncwarp();  // all lanes hold their entries of this block before misses overwrite it
 #pragma unroll
                 for (int k = 0; k < kBuIlp; ++k) {
@@ -633,10 +640,10 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
 #pragma unroll
                 for (int k = 0; k < kNbIlp; ++k) {
                     const int nv = min(dg[k] - first, 4);   // arcs of the block inside the row
-                    const bool h0 = nv > 0 && in_front(front, x[k].x);
-                    const bool h1 = nv > 1 && in_front(front, x[k].y);
-                    const bool h2 = nv > 2 && in_front(front, x[k].z);
-                    const bool h3 = nv > 3 && in_front(front, x[k].w);
+                    const bool h0 = nv > 0 && in_front_p(front, pk, x[k].x);
+                    const bool h1 = nv > 1 && in_front_p(front, pk, x[k].y);
+                    const bool h2 = nv > 2 && in_front_p(front, pk, x[k].z);
+                    const bool h3 = nv > 3 && in_front_p(front, pk, x[k].w);
                     const int kh = h0 ? 0 : h1 ? 1 : h2 ? 2 : h3 ? 3 : -1;
                     if (sv[k] >= 0) {
                         if (kh >= 0) {
@@ -716,7 +723,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                     const int64_t b = sj[s] & ~(int64_t)(kBuVec - 1);
 #pragma unroll
                     for (int k = 0; k < kBuVec; ++k)
-                        h[s][k] = sa[s] && b + k >= sj[s] && b + k < se[s] && in_front(front, a[s][k]);
+                        h[s][k] = sa[s] && b + k >= sj[s] && b + k < se[s] && in_front_p(front, pk, a[s][k]);
                 }
 #pragma unroll
                 for (int s = 0; s < kBuSlots; ++s) {
@@ -773,7 +780,7 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                 bool hh = false;
                 if (jj < je) {
                     uu = __ldg(adj + jj);
-                    hh = in_front(front, uu);
+                    hh = in_front_p(front, pk, uu);
                 }
                 const unsigned hm = __ballot_sync(kFull, hh);
                 if (hm) {
@@ -963,6 +970,16 @@ __global__ void k_emit_perm(const int2* __restrict__ rec, const int32_t* __restr
                             int64_t n_active, int64_t root_l, int32_t* __restrict__ depth,
                             int32_t* __restrict__ parent, const Ctl* ctl) {
     emit_perm_body(rec, label, n, n_active, ctl ? ctl->root_i : root_l, depth, parent);
+}
+
+// The bottom-up probes left the frontier bitmaps at L2 evict_last priority: back to
+// normal before the output pass streams its 9 GB (one thread per 128-byte line)
+__global__ void k_l2_demote(const uint32_t* a, const uint32_t* b, int64_t words) {
+    for (int64_t l = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; (l + 1) * 32 <= words;   // whole lines
+         l += (int64_t)gridDim.x * blockDim.x) {
+        l2_demote_line(a + l * 32);
+        l2_demote_line(b + l * 32);
+    }
 }
 
 // rec <- (-1, -1) for every vertex of [0, nbits) with degree > 0 that this search did
