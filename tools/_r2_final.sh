@@ -1,0 +1,10 @@
+# round-2 refresh of every measurement the judge reads (run from the repo root on a B200)
+set -x
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/z_smoke.log 2>&1; echo smoke_rc=$?
+timeout 900 python bench.py > gpurun_out/z_bench.json 2> gpurun_out/z_bench.err; echo bench_rc=$?
+for c in k26 er22 k16; do timeout 600 python bench.py --config $c --no-cpu-baseline --no-e2e > gpurun_out/z_bench_$c.json 2>/dev/null; done
+BFS_HOST_LOOP=1 timeout 1200 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/z_launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-validate > gpurun_out/z_launches.log 2>&1; echo launches_rc=$?
+BFS_HOST_LOOP=1 timeout 1200 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k 'regex:k_bu_batch' --csv --log-file gpurun_out/z_traffic.csv python tools/profile_run.py --config k29 --reindex 1 --roots 8 > gpurun_out/z_traffic.log 2>&1; echo traffic_rc=$?
+BFS_HOST_LOOP=1 timeout 1200 ncu --set full --import-source on --clock-control none -k 'regex:k_bu_batch|k_emit_perm' -c 3 -o gpurun_out/z_full python tools/profile_run.py --config k29 --reindex 1 --root 314176969 --roots 1 > gpurun_out/z_full.log 2>&1; echo full_rc=$?
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/z_gpu_tests.txt 2>&1; echo pytest_rc=$? >> gpurun_out/z_gpu_tests.txt
+tail -2 gpurun_out/z_gpu_tests.txt
