@@ -421,13 +421,12 @@ static void build_loop_graph(bfs_graph_s* g) {
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_td, B, 0, cudaGraphCondAssignDefault));
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_bu, B, 0, cudaGraphCondAssignDefault));
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_conv, B, 0, cudaGraphCondAssignDefault));
-    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step_begin, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_tds, h_td, h_bu,
-                                         h_conv);
+    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop, h_tds, h_td,
+                                         h_bu, h_conv);
     cudaGraph_t S = add_cond(B, {n_begin}, h_tds, cudaGraphCondTypeIf, &n_tds);
     cudaGraph_t T = add_cond(B, {n_begin}, h_td, cudaGraphCondTypeIf, &n_td);
     cudaGraph_t C = add_cond(B, {n_begin}, h_conv, cudaGraphCondTypeIf, &n_conv);   // BU from a queue
     cudaGraph_t U = add_cond(B, {n_conv}, h_bu, cudaGraphCondTypeIf, &n_bu);
-    add_kernel(B, {n_tds, n_td, n_bu}, k_step_end, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop);
     // small top-down step: one kernel
     add_kernel(S, {}, k_td_small, dim3(sms * 4), t256, 0, (const Ctl*)ctl, qa, qb, (const uint32_t*)g->front.p,
                (const uint32_t*)g->next.p, words, (const int64_t*)g->off.p, (const int32_t*)g->adj.p,
@@ -682,7 +681,7 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
         BFS_CUDA(cudaStreamSynchronize(s));
         R = reinterpret_cast<const LevelRec*>(g->h_lrec);
     }
-    // kernels the loop graph launched for step d (between k_step_begin and k_step_end)
+    // kernels the loop graph launched for step d (after its k_step)
     const int64_t tmin = g->tile_T ? tile_min_setting() : INT64_MAX, tsmall = td_small_setting(), cmin = td_claim_min();
     auto small = [&](int d) { return R[d].m_f <= tsmall && R[d].m_f <= 64 * R[d].n_f; };
     auto claimed = [&](int d) { return R[d].dir == 0 && !small(d) && (R[d].m_f >= cmin || R[d].m_f >= tmin); };
@@ -708,8 +707,9 @@ static bool bfs_run_graph(bfs_graph_s* g, int64_t root, int32_t* od, int32_t* op
             comp += L.kernel_ms;
         }
         g->levels.push_back(L);
-        launches += persistent ? 0 : 2 + step_kernels(d);
+        launches += persistent ? 0 : 1 + step_kernels(d);
     }
+    if (!persistent) ++launches;   // the last k_step, which ends the loop
     float ms = 0, ms_init = 0, ms_loop = 0;
     BFS_CUDA(cudaEventElapsedTime(&ms, g->ev[0], g->ev[1]));
     BFS_CUDA(cudaEventElapsedTime(&ms_init, g->ev[0], g->ev[2]));

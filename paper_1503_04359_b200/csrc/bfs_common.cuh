@@ -59,7 +59,7 @@ struct Ctl {
     long long claim_min;      // top-down steps with at least this many arcs run claim-only
     int claim, front_ok;      // this step is claim-only; the front bitmap holds the frontier
     long long tile_min;       // top-down steps with at least this many arcs run tiled (< 0: no tile index)
-    int tile, tile_pad;       // this step runs tiled (td_tile.cuh; implies claim)
+    int tile, started;        // this step runs tiled (td_tile.cuh; implies claim); a step has begun (k_step)
     long long td_small;       // top-down steps with at most this many arcs run as one kernel (k_td_small)
 };
 // one record per step, filled by the step kernels (times: %globaltimer ns)

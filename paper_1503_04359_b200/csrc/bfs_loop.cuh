@@ -1,4 +1,4 @@
-// Device-driven level loops: the loop-graph kernels (step begin / end,
+// Device-driven level loops: the loop-graph kernels (the step kernel,
 // TD / BU prologues, single-pass look-back scan) and the persistent one-kernel search.
 // Included once, inside namespace bfsb::{anonymous}, by bfs.cu (a single translation
 // unit: the kernels, device helpers and the host launch code share one file scope).
@@ -6,10 +6,10 @@
 
 // ============================================================ device-driven level loop
 // (SURVEY f3).  On one GPU the whole level loop is one CUDA graph: a WHILE node
-// whose body is k_step_begin (the alpha/beta decision, on the device) -> IF(top-down)
-// {k_td_prep -> k_scan_dev -> k_td_chunk_starts -> k_td_expand} and IF(bottom-up)
-// {k_bu_prep -> k_q2b_dev -> k_bu_batch} -> k_step_end (roll the counters, record
-// the step, continue while the frontier is non-empty).  The host launches it once
+// whose body is k_step (roll the counters of the step that just ran and record it,
+// then the alpha/beta decision on the device, or stop when the frontier is empty)
+// -> IF(top-down) {k_td_prep -> k_scan_dev -> k_td_chunk_starts -> k_td_expand} and
+// IF(bottom-up) {k_bu_prep -> k_q2b_dev -> k_bu_batch}.  The host launches it once
 // per search and synchronises once, instead of once per level.
 
 // init on the device: the root's internal label, visited <- skip | root, root
@@ -94,7 +94,7 @@ __device__ __forceinline__ long long step_decide(Ctl& c) {
     return m_u;
 }
 
-// the step's record and the roll of the counters into the loop state (k_step_end and
+// the step's record and the roll of the counters into the loop state (k_step and
 // the persistent kernel); returns whether the search continues
 __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned long long* cnt) {
     const long long next = (long long)cnt[C_NEXT], mf = (long long)cnt[C_MF];
@@ -129,10 +129,21 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
     return cont;
 }
 
-__global__ void k_step_begin(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_tds,
-                             cudaGraphConditionalHandle h_td, cudaGraphConditionalHandle h_bu,
-                             cudaGraphConditionalHandle h_conv) {
+// One kernel per level of the loop graph: the roll of the step that just ran (its record,
+// the counters into the loop state; nothing on the first call) and, if the search goes
+// on, the alpha/beta decision and the IF handles of the next step; otherwise the WHILE
+// handle drops to 0 and no IF body runs.  (Round 1 had a begin and an end kernel per
+// level: one single-thread launch more per level.)
+__global__ void k_step(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_loop,
+                       cudaGraphConditionalHandle h_tds, cudaGraphConditionalHandle h_td,
+                       cudaGraphConditionalHandle h_bu, cudaGraphConditionalHandle h_conv) {
     Ctl c = *ctl;
+    if (c.started && !step_finish(c, lrec[c.d], cnt)) {
+        *ctl = c;
+        cudaGraphSetConditional(h_loop, 0u);
+        return;   // the IF handles keep their default 0
+    }
+    c.started = 1;
     const long long t = gtimer();
     const long long m_u = step_decide(c);
     c.E = c.m_f;
@@ -238,12 +249,6 @@ __global__ void k_td_small(const Ctl* ctl, Queue qa, Queue qb, const uint32_t* _
     }
 }
 
-__global__ void k_step_end(Ctl* ctl, LevelRec* lrec, const unsigned long long* cnt, cudaGraphConditionalHandle h_loop) {
-    Ctl c = *ctl;
-    const bool cont = step_finish(c, lrec[c.d], cnt);
-    *ctl = c;
-    cudaGraphSetConditional(h_loop, cont ? 1u : 0u);
-}
 
 // top-down prologue: frontier bitmap -> queue when the previous step was bottom-up,
 // and a fresh tile state for the single-pass scan

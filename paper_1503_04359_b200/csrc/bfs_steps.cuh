@@ -451,7 +451,7 @@ constexpr int kBuCtas = 4;     // resident CTAs per SM (launch bound and grid; 5
 constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (aligned vector loads: 2, 4 or 8) and probes per round
-constexpr int kNbIlp = 2;     // listed rows per lane in flight in the second-probe phase
+constexpr int kNbIlp = 3;     // listed rows per lane in flight in the second-probe phase
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
 __global__ void __launch_bounds__(kBuWarps * 32, kBuCtas)
