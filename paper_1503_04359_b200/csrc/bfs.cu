@@ -413,20 +413,26 @@ static void build_loop_graph(bfs_graph_s* g) {
 
     cudaGraph_t G;
     BFS_CUDA(cudaGraphCreate(&G, 0));
-    cudaGraphConditionalHandle h_loop, h_tds, h_td, h_bu, h_conv;
+    cudaGraphConditionalHandle h_loop;
     BFS_CUDA(cudaGraphConditionalHandleCreate(&h_loop, G, 1, cudaGraphCondAssignDefault));
-    cudaGraphNode_t n_while, n_tds, n_td, n_bu, n_conv;
+    cudaGraphNode_t n_while, n_sw;
     cudaGraph_t B = add_cond(G, {}, h_loop, cudaGraphCondTypeWhile, &n_while);
-    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_tds, B, 0, cudaGraphCondAssignDefault));
-    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_td, B, 0, cudaGraphCondAssignDefault));
-    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_bu, B, 0, cudaGraphCondAssignDefault));
-    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_conv, B, 0, cudaGraphCondAssignDefault));
-    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop, h_tds, h_td,
-                                         h_bu, h_conv);
-    cudaGraph_t S = add_cond(B, {n_begin}, h_tds, cudaGraphCondTypeIf, &n_tds);
-    cudaGraph_t T = add_cond(B, {n_begin}, h_td, cudaGraphCondTypeIf, &n_td);
-    cudaGraph_t C = add_cond(B, {n_begin}, h_conv, cudaGraphCondTypeIf, &n_conv);   // BU from a queue
-    cudaGraph_t U = add_cond(B, {n_conv}, h_bu, cudaGraphCondTypeIf, &n_bu);
+    // one SWITCH node per level: body 0 small top-down, 1 top-down, 2 bottom-up after a
+    // queue -> bitmap conversion, 3 bottom-up (k_step selects; 4 = none, the last call)
+    cudaGraphConditionalHandle h_sw;
+    BFS_CUDA(cudaGraphConditionalHandleCreate(&h_sw, B, kStepNone, cudaGraphCondAssignDefault));
+    cudaGraphNode_t n_begin = add_kernel(B, {}, k_step, dim3(1), dim3(1), 0, ctl, lrec, cnt, h_loop, h_sw);
+    cudaGraph_t SW[4];
+    {
+        cudaGraphNodeParams cp{};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h_sw;
+        cp.conditional.type = cudaGraphCondTypeSwitch;
+        cp.conditional.size = 4;
+        BFS_CUDA(cudaGraphAddNode(&n_sw, B, &n_begin, 1, &cp));
+        for (int i = 0; i < 4; ++i) SW[i] = cp.conditional.phGraph_out[i];
+    }
+    cudaGraph_t S = SW[kStepSmallTd], T = SW[kStepTd], C = SW[kStepBuConv], U = SW[kStepBu];
     // small top-down step: one kernel
     add_kernel(S, {}, k_td_small, dim3(sms * 4), t256, 0, (const Ctl*)ctl, qa, qb, (const uint32_t*)g->front.p,
                (const uint32_t*)g->next.p, words, (const int64_t*)g->off.p, (const int32_t*)g->adj.p,
@@ -470,10 +476,12 @@ static void build_loop_graph(bfs_graph_s* g) {
     // bottom-up body
     // queue -> bitmap before a bottom-up step that follows a top-down one (IF node)
     cudaGraphNode_t u1 = add_kernel(C, {}, k_bu_prep, g8, t256, 0, ctl, g->front.p, g->next.p, words);
-    add_kernel(C, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
-    add_kernel(U, {}, k_bu_batch, dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p,
-               g->front.p, g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, bu_nb4(g), g->nb4_rows,
-               bu_nbp(g), words, g->lo, (int32_t)0, cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
+    cudaGraphNode_t u2 = add_kernel(C, {u1}, k_q2b_dev, g8, t256, 0, ctl, qa, qb, g->front.p, g->next.p);
+    for (cudaGraph_t X : {C, U})
+        add_kernel(X, X == C ? std::vector<cudaGraphNode_t>{u2} : std::vector<cudaGraphNode_t>{}, k_bu_batch,
+                   dim3(bu_grid), dim3(kBuWarps * 32), 0, g->off.p, g->head.p, g->adj.p, g->visited.p, g->front.p,
+                   g->next.p, g->rec.p, pmap, g->reindexed ? g->hpar.p : nullptr, bu_nb4(g), g->nb4_rows, bu_nbp(g),
+                   words, g->lo, (int32_t)0, cnt, grab, bu_long_setting(), bu_dense_setting(), ctl, lrec);
     BFS_CUDA(cudaGraphInstantiate(&g->loop_exec, G, 0));
     g->loop_graph = G;
 }

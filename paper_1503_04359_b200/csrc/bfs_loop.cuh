@@ -134,14 +134,14 @@ __device__ __forceinline__ bool step_finish(Ctl& c, LevelRec& r, const unsigned 
 // on, the alpha/beta decision and the IF handles of the next step; otherwise the WHILE
 // handle drops to 0 and no IF body runs.  (Round 1 had a begin and an end kernel per
 // level: one single-thread launch more per level.)
+enum { kStepSmallTd = 0, kStepTd = 1, kStepBuConv = 2, kStepBu = 3, kStepNone = 4 };
 __global__ void k_step(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGraphConditionalHandle h_loop,
-                       cudaGraphConditionalHandle h_tds, cudaGraphConditionalHandle h_td,
-                       cudaGraphConditionalHandle h_bu, cudaGraphConditionalHandle h_conv) {
+                       cudaGraphConditionalHandle h_sw) {
     Ctl c = *ctl;
     if (c.started && !step_finish(c, lrec[c.d], cnt)) {
         *ctl = c;
         cudaGraphSetConditional(h_loop, 0u);
-        return;   // the IF handles keep their default 0
+        return;   // the SWITCH handle keeps its default (no body)
     }
     c.started = 1;
     const long long t = gtimer();
@@ -163,10 +163,8 @@ __global__ void k_step(Ctl* ctl, LevelRec* lrec, unsigned long long* cnt, cudaGr
     lrec[c.d] = r;
     for (int i = 0; i < 8; ++i) cnt[i] = 0;
     *ctl = c;
-    cudaGraphSetConditional(h_tds, small ? 1u : 0u);
-    cudaGraphSetConditional(h_td, (c.dir == 0 && !small) ? 1u : 0u);
-    cudaGraphSetConditional(h_bu, c.dir == 1 ? 1u : 0u);
-    cudaGraphSetConditional(h_conv, (c.dir == 1 && c.have_queue && !c.front_ok) ? 1u : 0u);
+    cudaGraphSetConditional(h_sw, c.dir == 0 ? (small ? kStepSmallTd : kStepTd)
+                                             : ((c.have_queue && !c.front_ok) ? kStepBuConv : kStepBu));
 }
 
 // A small top-down step (m_f <= td_small arcs and at most 64 per frontier vertex: the
