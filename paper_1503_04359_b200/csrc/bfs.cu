@@ -116,7 +116,10 @@ static int64_t env_i64(const char* name, int64_t dflt) {
 static int64_t tile_min_setting() { return env_i64("BFS_TILE_MIN", (int64_t)1 << 24); }
 // top-down steps with at most this many arcs run as one kernel on the device loop
 // (k_td_small; BFS_TD_SMALL=-1 disables it)
-static int64_t td_small_setting() { return env_i64("BFS_TD_SMALL", (int64_t)1 << 15); }
+// top-down steps of at most this many arcs (and <= 64 per frontier vertex) run as the one
+// kernel k_td_small; 2^18 from the round-2 sweep (ER22 +2.2%, K26 +0.6%, K29 +0.1% vs 2^15;
+// 2^22 loses: profiles/r02_td_small_sweep.txt)
+static int64_t td_small_setting() { return env_i64("BFS_TD_SMALL", (int64_t)1 << 18); }
 
 TileLog tile_log(const bfs_graph_s* g) {
     return TileLog{g->tile_pool.p, g->tile_ubase.p, g->tile_ucnt.p, g->tile_lpool.p, g->tile_lcnt.p,
