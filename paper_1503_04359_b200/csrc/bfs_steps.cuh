@@ -451,7 +451,7 @@ constexpr int kBuCtas = 4;     // resident CTAs per SM (launch bound and grid; 5
 constexpr int kBuSlots = 3;
 constexpr int kBuIlp = 8;
 constexpr int kBuVec = 4;      // arcs a slot reads (aligned vector loads: 2, 4 or 8) and probes per round
-constexpr int kNbIlp = 3;     // listed rows per lane in flight in the second-probe phase
+constexpr int kNbIlp = 4;     // listed rows per lane in flight in the second-probe phase
 constexpr int kLongCap = 16;   // small: shared memory left to L1 matters more (B200-measured)
 
 __global__ void __launch_bounds__(kBuWarps * 32, kBuCtas)
@@ -624,7 +624,9 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
             const int first = 1 + 4 * pl;
             int M2 = 0;
             for (int t0 = 0; t0 < M; t0 += 32 * kNbIlp) {
-                int32_t sv[kNbIlp], dg[kNbIlp];
+                // the block's -1 padding marks the row's end, so only the block is loaded
+                // (the degree is read for the hits alone, for m_f)
+                int32_t sv[kNbIlp];
                 int4 x[kNbIlp];
 #pragma unroll
                 for (int k = 0; k < kNbIlp; ++k) {
@@ -632,18 +634,15 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                     sv[k] = idx < M ? (int32_t)list[idx] : -1;
                 }
 #pragma unroll
-                for (int k = 0; k < kNbIlp; ++k) {
-                    dg[k] = sv[k] >= 0 ? __ldg(head + vbase + sv[k]).y : 0;
+                for (int k = 0; k < kNbIlp; ++k)
                     x[k] = sv[k] >= 0 ? __ldg(pb + vbase + sv[k]) : make_int4(-1, -1, -1, -1);
-                }
                 __syncwarp();  // the block is in registers before survivors overwrite it
 #pragma unroll
                 for (int k = 0; k < kNbIlp; ++k) {
-                    const int nv = min(dg[k] - first, 4);   // arcs of the block inside the row
-                    const bool h0 = nv > 0 && in_front_p(front, pk, x[k].x);
-                    const bool h1 = nv > 1 && in_front_p(front, pk, x[k].y);
-                    const bool h2 = nv > 2 && in_front_p(front, pk, x[k].z);
-                    const bool h3 = nv > 3 && in_front_p(front, pk, x[k].w);
+                    const bool h0 = x[k].x >= 0 && in_front_p(front, pk, x[k].x);
+                    const bool h1 = x[k].y >= 0 && in_front_p(front, pk, x[k].y);
+                    const bool h2 = x[k].z >= 0 && in_front_p(front, pk, x[k].z);
+                    const bool h3 = x[k].w >= 0 && in_front_p(front, pk, x[k].w);
                     const int kh = h0 ? 0 : h1 ? 1 : h2 ? 2 : h3 ? 3 : -1;
                     if (sv[k] >= 0) {
                         if (kh >= 0) {
@@ -651,12 +650,15 @@ k_bu_batch(const int64_t* __restrict__ off, const int2* __restrict__ head, const
                             my_insp += (unsigned long long)(kh + 1);
                             __stcs(out + vbase + sv[k], make_int2(next_level, pmap ? pmap[hu] : hu));
                             atomicOr(nbw + (sv[k] >> 5), 1u << (sv[k] & 31));
-                            my_mf += (unsigned long long)dg[k];
+                            my_mf += (unsigned long long)__ldg(head + vbase + sv[k]).y;
                         } else {
-                            my_insp += (unsigned long long)nv;
+                            my_insp += (unsigned long long)((x[k].x >= 0) + (x[k].y >= 0) + (x[k].z >= 0) +
+                                                            (x[k].w >= 0));
                         }
                     }
-                    const bool miss = sv[k] >= 0 && kh < 0 && dg[k] > first + 4;
+                    // a full block without a hit: the row may go on (a row of exactly
+                    // first + 4 arcs ends with an empty block or at once in 3b)
+                    const bool miss = sv[k] >= 0 && kh < 0 && x[k].w >= 0;
                     const unsigned mm = __ballot_sync(kFull, miss);
                     if (miss) list[M2 + __popc(mm & lanemask_lt())] = (uint16_t)sv[k];
                     M2 += __popc(mm);
