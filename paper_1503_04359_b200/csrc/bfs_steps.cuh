@@ -194,9 +194,10 @@ k_td_expand(const Queue q_in, const int64_t* __restrict__ prefix, const int64_t*
         // queue are produced in vertex order by k_td_finish
         if (claim_only) {
             if (use_log) {
+                int32_t pj[kTdItems];
 #pragma unroll
-                for (int j = 0; j < kTdItems; ++j)
-                    light_log(lg, win[j], v[j], win[j] ? (pmap ? __ldg(pmap + u[j]) : u[j]) : 0);
+                for (int j = 0; j < kTdItems; ++j) pj[j] = win[j] ? (pmap ? __ldg(pmap + u[j]) : u[j]) : 0;
+                light_log_all<kTdItems>(lg, win, v, pj);
             } else {
 #pragma unroll
                 for (int j = 0; j < kTdItems; ++j)

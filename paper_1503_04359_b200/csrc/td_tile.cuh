@@ -107,23 +107,44 @@ struct TileLog {
 
 // light-row winner's record into its (tile, window) bucket; every lane of the calling
 // (possibly partial) warp must call it, `win` says whether it has a record
-__device__ __forceinline__ void light_log(const TileLog& lg, bool win, int32_t v, int32_t par) {
-    const unsigned act = __activemask();
-    const unsigned m = __ballot_sync(act, win);
-    if (!win) return;
+__device__ __forceinline__ int light_window(const TileLog& lg, int32_t v) {
     int t = 0, hi_ = lg.T - 1;   // tile of v (global starts: binary search)
     while (t < hi_) {
         const int m = (t + hi_ + 1) >> 1;
         if (__ldg(lg.ts + m) <= v) t = m;
         else hi_ = m - 1;
     }
-    const int w = __ldg(lg.wf + t) + ((v - __ldg(lg.ts + t)) >> kWinShift);
-    const unsigned peers = __match_any_sync(m, w);
-    const int leader = __ffs(peers) - 1;
-    unsigned pos = 0;
-    if ((int)(threadIdx.x & 31) == leader) pos = atomicAdd(lg.lcnt + w, (unsigned)__popc(peers));
-    pos = __shfl_sync(peers, pos, leader) + __popc(peers & lanemask_lt());
-    lg.lpool[((int64_t)w << kWinShift) + pos] = make_int2(v, par);
+    return __ldg(lg.wf + t) + ((v - __ldg(lg.ts + t)) >> kWinShift);
+}
+// All kN items of a thread at once: the windows first, then one warp-aggregated
+// atomicAdd per (item, window group) with every item's atomic in flight before any
+// result is used, then the stores -- one atomic round trip per call instead of kN.
+template <int kN>
+__device__ __forceinline__ void light_log_all(const TileLog& lg, const bool (&win)[kN], const int32_t (&v)[kN],
+                                              const int32_t (&par)[kN]) {
+    const unsigned act = __activemask();
+    const int lane = threadIdx.x & 31;
+    int w[kN];
+#pragma unroll
+    for (int j = 0; j < kN; ++j) w[j] = win[j] ? light_window(lg, v[j]) : 0;
+    unsigned peers[kN], base[kN];
+#pragma unroll
+    for (int j = 0; j < kN; ++j) {
+        const unsigned m = __ballot_sync(act, win[j]);
+        peers[j] = 0u;
+        base[j] = 0u;
+        if (win[j]) {
+            peers[j] = __match_any_sync(m, w[j]);
+            if (lane == __ffs(peers[j]) - 1) base[j] = atomicAdd(lg.lcnt + w[j], (unsigned)__popc(peers[j]));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < kN; ++j) {
+        if (win[j]) {
+            const unsigned pos = __shfl_sync(peers[j], base[j], __ffs(peers[j]) - 1) + __popc(peers[j] & lanemask_lt());
+            lg.lpool[((int64_t)w[j] << kWinShift) + pos] = make_int2(v[j], par[j]);
+        }
+    }
 }
 
 // The heavy frontier vertices (label < nh) of the current queue into hlist (count
