@@ -293,11 +293,22 @@ __device__ __forceinline__ void td_finish_body(const uint32_t* __restrict__ visi
         }
         my_n += (unsigned long long)__popc(nb);
         unsigned todo = __ballot_sync(kFull, nb != 0u);
-        while (todo) {   // word by word: the 32 lanes read 32 consecutive head records
-            const int k = __ffs(todo) - 1;
-            todo &= todo - 1;
-            const uint32_t nk = __shfl_sync(kFull, nb, k);
-            if ((nk >> lane) & 1u) my_mf += (unsigned long long)__ldg(head + (b0 + k) * 32 + lane).y;
+        while (todo) {   // word by word: the 32 lanes read 32 consecutive head records,
+                         // 4 words' loads in flight before any is summed
+            constexpr int kW = 4;
+            int32_t dg[kW];
+#pragma unroll
+            for (int q = 0; q < kW; ++q) {
+                dg[q] = 0;
+                if (todo) {
+                    const int k = __ffs(todo) - 1;
+                    todo &= todo - 1;
+                    const uint32_t nk = __shfl_sync(kFull, nb, k);
+                    if ((nk >> lane) & 1u) dg[q] = __ldg(head + (b0 + k) * 32 + lane).y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kW; ++q) my_mf += (unsigned long long)dg[q];
         }
     }
     my_mf = warp_sum_u64(my_mf);
