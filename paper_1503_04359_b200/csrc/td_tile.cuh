@@ -359,11 +359,18 @@ k_tile_rec(const Ctl* ctl, int32_t level_in, const int2* __restrict__ wl, const 
         const unsigned n = light ? lg.lcnt[blockIdx.x] : lg.cnt[(int64_t)u * kMaxWin + k];
         const int2* P = light ? lg.lpool + ((int64_t)blockIdx.x << kWinShift)
                               : lg.pool + lg.base[u] + ((int64_t)k << kWinShift);
-        for (unsigned i = threadIdx.x; i < n; i += kWinThreads) {
-            const int2 e = __ldcs(P + i);
-            // a vertex two parts of a split tile both claimed has two (valid) entries: the
-            // larger parent label wins, deterministically
-            atomicMax(s_p + (e.x - v0), e.y);
+        // a vertex two parts of a split tile both claimed has two (valid) entries: the
+        // larger parent label wins, deterministically.  4 entries per thread in flight.
+        for (unsigned i0 = threadIdx.x; i0 < n; i0 += 4 * kWinThreads) {
+            int2 e[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const unsigned i = i0 + q * kWinThreads;
+                e[q] = i < n ? __ldcs(P + i) : make_int2(-1, 0);
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (e[q].x >= 0) atomicMax(s_p + (e[q].x - v0), e[q].y);
         }
     }
     __syncthreads();
