@@ -23,6 +23,7 @@ ap.add_argument("--root", type=int, default=-1, help="run this root (original la
 ap.add_argument("--reindex", type=int, default=0)
 ap.add_argument("--alpha", type=int, default=30)
 ap.add_argument("--beta", type=int, default=1000)
+ap.add_argument("--reps", type=int, default=1, help="run the root list this many times")
 a = ap.parse_args()
 cfg = bench.CONFIGS[a.config]
 torch.cuda.set_device(0)
@@ -30,6 +31,7 @@ g = pkg.Graph.kronecker(cfg["scale"], cfg["ef"], cfg["seed"], cfg["abc"],
                         opts=pkg.default_opts(reindex_by_degree=bool(a.reindex)))
 print("build_ms", g.build_ms, flush=True)
 roots = [a.root] if a.root >= 0 else g.sample_roots(cfg["scale"], cfg["seed"], a.skip + a.roots)[a.skip:]
+roots = list(roots) * a.reps
 g.set_policy(mode=a.mode, alpha=a.alpha, beta=a.beta, level_times=True)
 for r in roots:
     p, d = g.run(int(r))
