@@ -20,6 +20,7 @@ import paper_1503_04359_b200 as pkg  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=6)
 ap.add_argument("--roots", type=int, default=64)
+ap.add_argument("--no-output", action="store_true", help="searches without the output pass (null outputs)")
 a = ap.parse_args()
 cfg = bench.CONFIGS["k29"]
 torch.cuda.set_device(0)
@@ -31,7 +32,10 @@ depth = torch.empty(g.n, dtype=torch.int32, device="cuda")
 res = {int(r): [] for r in roots}
 for rep in range(a.reps):
     for r in roots:
-        pkg.bfs_run(g.h, int(r), parent, depth)
+        if a.no_output:
+            pkg.bfs_run(g.h, int(r), None, None)
+        else:
+            pkg.bfs_run(g.h, int(r), parent, depth)
         run, levels = g.stats(tuples=False)
         res[int(r)].append((run["ms_total"], [(lv["direction"], round(lv["ms"], 3), round(lv["kernel_ms"], 3)) for lv in levels]))
 out = []
