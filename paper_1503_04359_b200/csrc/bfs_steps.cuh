@@ -937,9 +937,35 @@ __device__ __forceinline__ void emit_perm_body(const int2* __restrict__ rec, con
     const int lane = threadIdx.x & 31;
     const int64_t tiles = (n + 32 * kEmitV - 1) / (32 * kEmitV);
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    // 32-byte aligned outputs: lane i takes the 8 consecutive vertices 8i..8i+7 of the
+    // tile, one 256-bit label load and two 256-bit stores (half the memory instructions
+    // of the 16-byte path below)
+    const bool vec8 = ((reinterpret_cast<uintptr_t>(depth) | reinterpret_cast<uintptr_t>(parent) |
+                        reinterpret_cast<uintptr_t>(label)) & 31) == 0 && depth && parent && kEmitV == 8;
     for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < tiles; t += nwarps) {
         const int64_t t0 = t * 32 * kEmitV;
         const bool full = t0 + 32 * kEmitV <= n;
+        if (vec8 && full) {
+            const int64_t v0 = t0 + lane * 8;
+            int32_t iv[8];
+            asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                         : "=r"(iv[0]), "=r"(iv[1]), "=r"(iv[2]), "=r"(iv[3]), "=r"(iv[4]), "=r"(iv[5]), "=r"(iv[6]),
+                           "=r"(iv[7])
+                         : "l"(label + v0));
+            int2 o[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const bool act = iv[k] >= 0 && (iv[k] < n_active || iv[k] == root_l);
+                o[k] = act ? __ldg(rec + iv[k]) : make_int2(-1, -1);
+            }
+            asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(depth + v0), "r"(o[0].x),
+                         "r"(o[1].x), "r"(o[2].x), "r"(o[3].x), "r"(o[4].x), "r"(o[5].x), "r"(o[6].x), "r"(o[7].x)
+                         : "memory");
+            asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(parent + v0), "r"(o[0].y),
+                         "r"(o[1].y), "r"(o[2].y), "r"(o[3].y), "r"(o[4].y), "r"(o[5].y), "r"(o[6].y), "r"(o[7].y)
+                         : "memory");
+            continue;
+        }
         int32_t iv[kEmitV];
 #pragma unroll
         for (int h = 0; h < kEmitV / 4; ++h) {
