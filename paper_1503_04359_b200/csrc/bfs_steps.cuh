@@ -948,7 +948,7 @@ __device__ __forceinline__ void emit_perm_body(const int2* __restrict__ rec, con
         if (vec8 && full) {
             const int64_t v0 = t0 + lane * 8;
             int32_t iv[8];
-            asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            asm volatile("ld.global.nc.L1::no_allocate.L2::evict_first.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                          : "=r"(iv[0]), "=r"(iv[1]), "=r"(iv[2]), "=r"(iv[3]), "=r"(iv[4]), "=r"(iv[5]), "=r"(iv[6]),
                            "=r"(iv[7])
                          : "l"(label + v0));
